@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""bench.py -- embeddings/s of the Delta-Motif hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c5] [--impl reference]
+
+A "step" is one full dm_match of the workload (seed -> every join step -> count), i.e. one
+pass of the whole hot path.  Default workload (BASELINE config 5, the configuration the
+metric's 1/2/4/8-GPU scaling is quoted on that fits one GPU): 30-vertex path pattern into the
+IBM heavy-hex family w=31 (9,983 vertices / 11,904 edges), count mode.
+
+value   = embeddings found by all ranks per second of device time, timed with CUDA events on
+          the launching stream around each step (max over ranks), L2 flushed between steps.
+e2e     = the same metric through the public API from pinned HOST buffers: dm_graph_create
+          (H2D of the edge list, CSR build) + dm_match + D2H of the count, per step.
+roofline= the dominant kernel (k_step count or write pass) against the measured HBM peak,
+          with the SURVEY §8(d) algorithmic byte model.
+cpu_baseline = the CPU oracle (test infrastructure, plain backtracking) on a bounded root
+          sample of the same workload on this host's cores.
+
+Multi-GPU: launched by torchrun; the graph is replicated, the seed vertices are cut into
+equal-work ranges (paper_2508_21287_b200.dist), counts are all_reduced over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import dm_inputs as gen  # noqa: E402
+
+METRIC = "embeddings/sec (device-timed, max over ranks) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "embeddings/s"
+
+WORKLOADS = {
+    # name: (description, data graph builder, pattern builder, drop self loops)
+    "c5": ("config5: P30 path into IBM heavy-hex w=31 (9983 V, 11904 E), count",
+           lambda: gen.ibm_heavy_hex(31), lambda: gen.path(30), False),
+    "c4-diamond": ("config4: diamond into R-MAT scale 20 edge factor 16, count",
+                   lambda: gen.rmat(20, 16, seed=1), gen.diamond, True),
+    "c4-k4": ("config4: 4-clique into R-MAT scale 20 edge factor 16, count",
+              lambda: gen.rmat(20, 16, seed=1), lambda: gen.clique(4), True),
+    "c3-p20": ("config3: P20 into IBM heavy-hex w=10 (1121 V), count",
+               lambda: gen.ibm_heavy_hex(10), lambda: gen.path(20), False),
+    "c2-er-c4": ("config2: C4 into ER G(1e4, 8e4) seed 1, count",
+                 lambda: gen.er_gnm(10_000, 80_000, 1), lambda: gen.ring(4), False),
+}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+def cpu_baseline(n, e, k, pe, drop, target_s=12.0):
+    """The oracle as it stands on a bounded root sample (f(order[0]) in [0, R))."""
+    import oracle
+    threads = os.cpu_count() or 1
+    R = max(1, min(n, 64))
+    while True:
+        r = oracle.match(n, e, k, pe, table=False, drop_self_loops=drop, roots=(0, R), threads=threads)
+        if r.seconds >= target_s / 4 or R >= n:
+            break
+        grow = max(2.0, (target_s / max(r.seconds, 1e-3)))
+        R = int(min(n, R * grow))
+    if r.seconds < target_s / 2 and R < n:
+        R = int(min(n, R * (target_s / max(r.seconds, 1e-3))))
+        r = oracle.match(n, e, k, pe, table=False, drop_self_loops=drop, roots=(0, R), threads=threads)
+    return {"value": r.count / max(r.seconds, 1e-9), "unit": UNIT, "cores": r.threads,
+            "kind": "oracle",
+            "sample": f"roots f(v{int(r.order[0])}) in [0,{R}) of {n} data vertices "
+                      f"({100.0 * R / max(n, 1):.1f}% of the root set): {r.count} embeddings "
+                      f"in {r.seconds:.2f}s on {r.threads} threads"}, r
+
+
+def run_reference(args, wl):
+    """--impl reference: the CPU oracle (this tier's reference arm) on bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    desc, gfn, pfn, drop = WORKLOADS[wl]
+    n, e = gfn()
+    k, pe = pfn()
+    per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    base, _ = cpu_baseline(n, e, k, pe, drop, target_s=per_step)
+    vals = []
+    import oracle
+    R = int(base["sample"].split("[0,")[1].split(")")[0])
+    threads = os.cpu_count() or 1
+    tot_s = 0.0
+    for i in range(args.warmup + args.steps):
+        r = oracle.match(n, e, k, pe, table=False, drop_self_loops=drop, roots=(0, R), threads=threads)
+        if i >= args.warmup:
+            vals.append(r.count / max(r.seconds, 1e-9))
+            tot_s += r.seconds
+    v = statistics.median(vals) if vals else base["value"]
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1000.0 * tot_s / max(1, args.steps), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+           "config": {"workload": desc, "sample": base["sample"]},
+           "cpu_baseline": {**base, "value": v},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args, args.workload)
+
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2508_21287_b200 as dm
+    from paper_2508_21287_b200.dist import equal_work_cuts
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist_on = world > 1
+    if dist_on:
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    desc, gfn, pfn, drop = WORKLOADS[args.workload]
+    n, e = gfn()
+    k, pe = pfn()
+
+    stream = torch.cuda.current_stream()
+    t0 = time.perf_counter()
+    G = dm.Graph(n, e, drop_self_loops=drop, device=local)
+    prep_s = time.perf_counter() - t0
+    off, _ = G.csr()
+    cuts = equal_work_cuts(off, world)
+    seed = (cuts[rank], cuts[rank + 1])
+    plan = dm.Plan(k, pe)
+    flush = torch.empty(int(300e6) // 4, dtype=torch.int32, device="cuda")  # > 126 MB L2
+
+    def barrier():
+        if dist_on:
+            tdist.barrier()
+        torch.cuda.synchronize()
+
+    def one(profile=False):
+        return G.match(k, pe, seed_range=seed, stream=stream, profile=profile)
+
+    for _ in range(max(3, args.warmup)):
+        one()
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    times, stats, count = [], [], 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        r = one(profile=True)
+        ev[i][1].record(stream)
+        count += r.count
+        stats.append(r.stats)
+    barrier()
+    clocks = clk.stop()
+    times = [a.elapsed_time(b) for a, b in ev]
+    local_ms = float(sum(times))
+    t = torch.tensor([local_ms, float(count)], dtype=torch.float64, device="cuda")
+    if dist_on:
+        mx = t.clone()
+        tdist.all_reduce(mx, op=tdist.ReduceOp.MAX)
+        sm = t.clone()
+        tdist.all_reduce(sm, op=tdist.ReduceOp.SUM)
+        max_ms, total_count = float(mx[0]), float(sm[1])
+    else:
+        max_ms, total_count = local_ms, float(count)
+    value = total_count / (max_ms / 1000.0)
+
+    # ---------------- roofline of the dominant kernel (SURVEY §8(d) byte model)
+    kinds = {"k_step<count>": [0.0, 0.0, 0], "k_step<write>": [0.0, 0.0, 0]}
+    for s in stats:
+        for i in range(s["num_steps"]):
+            win = 0 if i == 0 else s["width_in"][i]
+            read = 4.0 * win * s["rows_in"][i] + 8.0 * s["rows_in"][i] + 4.0 * s["candidates"][i] + 4.0 * s["probes"][i]
+            last_count = (i == s["num_steps"] - 1)
+            kinds["k_step<count>"][0] += s["ms_count"][i]
+            kinds["k_step<count>"][1] += read
+            kinds["k_step<count>"][2] += 1
+            if not last_count:
+                kinds["k_step<write>"][0] += s["ms_write"][i]
+                kinds["k_step<write>"][1] += read + 4.0 * s["width_out"][i] * s["rows_out"][i]
+                kinds["k_step<write>"][2] += 1
+    dom = max(kinds, key=lambda kk: kinds[kk][0])
+    ms, byts, launches = kinds[dom]
+    peak, peak_src = load_peaks()
+    achieved = (byts / 1e9) / (ms / 1e3) if ms > 0 else 0.0
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+        except Exception:
+            traffic = None
+    total_model = sum(sum(s["bytes_model"]) for s in stats)
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "traffic": traffic,
+            "bytes_per_launch": byts / max(1, launches), "ms_per_launch": ms / max(1, launches),
+            "peak_source": peak_src, "kernel_share_of_step": ms / max(1e-9, sum(times)),
+            "step_model_GBps": (total_model / 1e9) / (sum(times) / 1e3),
+            "bytes_model_per_embedding": total_model / max(1.0, float(count))}
+
+    # ---------------- end to end through the public API from pinned host buffers
+    e2e_val = None
+    h2d = d2h = 0
+    if args.e2e_steps > 0:
+        pin = torch.from_numpy(np.ascontiguousarray(e)).pin_memory()
+        epin = pin.numpy()
+        for _ in range(2):
+            G2 = dm.Graph(n, epin, drop_self_loops=drop, device=local)
+            G2.match(k, pe, seed_range=seed, stream=stream)
+            G2.close()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ecount = 0
+        for _ in range(args.e2e_steps):
+            G2 = dm.Graph(n, epin, drop_self_loops=drop, device=local)
+            r2 = G2.match(k, pe, seed_range=seed, stream=stream)
+            ecount += r2.count
+            G2.close()
+        b.record(stream)
+        barrier()
+        ems = a.elapsed_time(b)
+        t2 = torch.tensor([ems, float(ecount)], dtype=torch.float64, device="cuda")
+        if dist_on:
+            m2 = t2.clone()
+            tdist.all_reduce(m2, op=tdist.ReduceOp.MAX)
+            s2 = t2.clone()
+            tdist.all_reduce(s2, op=tdist.ReduceOp.SUM)
+            ems, ecount = float(m2[0]), float(s2[1])
+        e2e_val = ecount / (ems / 1000.0)
+        h2d = int(e.nbytes)
+        d2h = 8 * (plan.num_steps + 1) + 8 * (1 + 2 * plan.num_steps)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu, _ = cpu_baseline(n, e, k, pe, drop)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": max(3, args.warmup),
+               "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+               "config": {"workload": desc, "embeddings_per_step": int(total_count / args.steps),
+                          "data_graph_vertices": n, "data_graph_edges": int(len(e)),
+                          "pattern_vertices": k, "mode": "count (monomorphism)",
+                          "motifs": "M3-O,M3,M2", "plan_steps": plan.num_steps,
+                          "l2_flush": "300 MB buffer written between timed steps",
+                          "parallelism": f"seed-shard x{world} (replicated graph)",
+                          "prep_ms_graph_create": prep_s * 1e3},
+               "roofline": roof, "cpu_baseline": cpu,
+               "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": d2h},
+               "gpu_launches": int(sum(s["num_launches"] for s in stats)),
+               "clocks": clocks}
+        print(json.dumps(out), flush=True)
+    if dist_on:
+        tdist.barrier()
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

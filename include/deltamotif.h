@@ -1,0 +1,185 @@
+/*
+ * deltamotif.h -- C ABI of libdeltamotif.so, the B200-native (sm_100a) hot path of
+ * Delta-Motif (arXiv 2508.21287, "Subgraph Isomorphism at Scale via Data-Centric
+ * Parallelism").  Citations: P:n = PAPER.md line n; S:n = SPEC.md line n.
+ *
+ * What the library computes (§3.1): for a data graph G_d and a connected pattern G_p,
+ * every injective map f : V_p -> V_d with (u,v) in E_p => (f(u),f(v)) in E_d (DM_MONO, the
+ * join-and-filter pipeline of §3.2, and §3.4) or with <=> for every pattern
+ * pair (DM_INDUCED, the literal reading of P:167).  It gets there the paper's way: both
+ * graphs become edge tables, the pattern is decomposed into motif slices (§3.3),
+ * and a table of partial embeddings is grown by equi-joins with the motif tables followed by
+ * the overlapping-node filter (Alg. 1).  Each join step is one fused sm_100a kernel
+ * pair (count, then write), see DESIGN.md.
+ *
+ * Conventions
+ *  - Vertex ids are int32 in [0, n); counts are uint64; row offsets int64.
+ *  - All functions are thread-safe.  A dm_graph is immutable after creation and may be
+ *    matched concurrently from several host threads / CUDA streams.
+ *  - Errors: every dm_status-returning call returns DM_OK (0) or a negative code and sets a
+ *    thread-local message readable with dm_last_error().  Nothing is written to stderr.
+ *    Output pointers are left untouched (NULL) on error.
+ *  - Host pointers are read during the call only (copied); device memory is owned by the
+ *    handle that allocated it.
+ *  - No CPU fallback: every computational entry point requires a CUDA device; without one it
+ *    returns DM_ERR_CUDA.
+ */
+#ifndef DELTAMOTIF_H
+#define DELTAMOTIF_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define DM_API __attribute__((visibility("default")))
+#else
+#define DM_API
+#endif
+
+#define DM_ABI_VERSION 1
+#define DM_MAX_PATTERN 64 /* max pattern vertices k */
+
+typedef struct dm_graph dm_graph;   /* device CSR of G_d (Res(M2), both orientations) */
+typedef struct dm_result dm_result; /* count + optional canonical host table + stats   */
+typedef struct dm_plan dm_plan;     /* host join program (decomposition + steps)       */
+
+typedef enum {
+  DM_OK = 0,
+  DM_ERR_ARG = -1,                  /* NULL pointer, negative size, bad option value       */
+  DM_ERR_VERTEX_RANGE = -2,         /* edge endpoint outside [0, n)                 */
+  DM_ERR_SELF_LOOP = -3,            /* self-loop in G_d without DM_GRAPH_DROP_SELF_LOOPS, or
+                                       any self-loop in G_p ("excluding self-loops") */
+  DM_ERR_PATTERN_DISCONNECTED = -4, /* G_p not connected             */
+  DM_ERR_OOM = -5,                  /* device or host allocation failed                    */
+  DM_ERR_ROW_BUDGET = -6,           /* table mode: result larger than row_budget   */
+  DM_ERR_CUDA = -7,                 /* CUDA runtime error / no device                      */
+  DM_ERR_UNSUPPORTED = -8           /* k > DM_MAX_PATTERN, ...                             */
+} dm_status;
+
+enum { DM_MONO = 0, DM_INDUCED = 1 };                      /* isomorphism variant (DESIGN Q1) */
+enum { DM_OUT_COUNT = 1, DM_OUT_TABLE = 2 };               /* output bit flags                */
+enum { DM_MOTIF_M2 = 1, DM_MOTIF_M3 = 2, DM_MOTIF_M3O = 4 }; /* planner motif set (bitmask);
+                                                              M2 = edge, M3 = wedge (2-path),
+                                                              M3-O = triangle        */
+enum { DM_GRAPH_DROP_SELF_LOOPS = 1 };                     /* dm_graph_create flags           */
+enum { DM_MATCH_PROFILE = 1 };                             /* dm_match_opts.flags: time every
+                                                              kernel with CUDA events          */
+
+typedef struct {
+  int32_t mode;        /* DM_MONO (default) or DM_INDUCED                                     */
+  int32_t output;      /* DM_OUT_COUNT and/or DM_OUT_TABLE (default DM_OUT_COUNT)             */
+  int32_t motifs;      /* planner motif set, bitmask of DM_MOTIF_*; M2 is always added*/
+  int32_t flags;       /* DM_MATCH_PROFILE ...                                                */
+  uint64_t row_budget; /* table mode: max result rows, 0 -> 2^27                      */
+  uint64_t mem_budget; /* bytes for one materialized frontier chunk, 0 -> auto (free/4)       */
+  int64_t seed_begin;  /* shard of the seed: the first plan vertex ranges over data vertices  */
+  int64_t seed_end;    /*   [seed_begin, seed_end); seed_end < 0 means n (whole graph)         */
+  void *cuda_stream;   /* cudaStream_t to launch on; NULL = legacy default stream             */
+} dm_match_opts;
+
+/* Per-match statistics (DM_MATCH_PROFILE fills the timing fields). */
+#define DM_MAX_STEPS 64
+typedef struct {
+  int32_t num_steps;             /* executed join steps (seed included)                    */
+  int32_t num_launches;          /* kernels launched by this dm_match call                 */
+  int32_t num_chunks;            /* frontier chunks processed (>= num_steps when chunked)  */
+  int32_t reserved;
+  uint64_t rows_in[DM_MAX_STEPS];    /* |F_i| summed over chunks                           */
+  uint64_t rows_out[DM_MAX_STEPS];   /* |F_{i+1}| (survivors)                              */
+  uint64_t candidates[DM_MAX_STEPS]; /* C_i: join matches before filters (first new vertex,
+                                        plus second-level matches for 2-vertex steps)      */
+  uint64_t probes[DM_MAX_STEPS];     /* Q_i: closing-edge / non-edge probe targets         */
+  int32_t width_in[DM_MAX_STEPS];    /* w_i                                                */
+  int32_t width_out[DM_MAX_STEPS];   /* w_{i+1}                                            */
+  double bytes_model[DM_MAX_STEPS];  /* SURVEY §8(d) algorithmic bytes of step i           */
+  double ms_count[DM_MAX_STEPS];     /* device ms in count-pass kernels of step i          */
+  double ms_write[DM_MAX_STEPS];     /* device ms in write-pass kernels of step i          */
+  double ms_other;                   /* scans, canonical sort, copies                      */
+  double ms_total;                   /* device ms from first to last launch                */
+} dm_match_stats;
+
+/* Fill *opt with defaults (DM_MONO, DM_OUT_COUNT, all motifs, whole graph, NULL stream). */
+DM_API void dm_match_opts_init(dm_match_opts *opt);
+
+/* ABI version (DM_ABI_VERSION) -- lets bindings detect a stale library. */
+DM_API int32_t dm_abi_version(void);
+
+/*
+ * dm_graph_create -- build Res(M2) = E_d \ E_self in both orientations (Alg. 2
+ * l.2) as a device CSR: int64 off[n+1], int32 adj[2m'] with every adjacency list sorted
+ * ascending; duplicates and reversed pairs collapse.
+ *   n      number of data vertices (>= 0)
+ *   edges  HOST array int32[m][2] of undirected edges (row-major pairs); may be NULL if m == 0
+ *   flags  DM_GRAPH_DROP_SELF_LOOPS: drop (u,u) instead of failing with DM_ERR_SELF_LOOP
+ *   device CUDA device ordinal the CSR lives on
+ *   out    receives the handle (free with dm_graph_destroy)
+ * Errors: DM_ERR_ARG, DM_ERR_VERTEX_RANGE, DM_ERR_SELF_LOOP, DM_ERR_OOM, DM_ERR_CUDA.
+ * The build runs on device (sort, dedup, degree scan) and is the "data preparation" phase
+ * the paper times separately.
+ */
+DM_API dm_status dm_graph_create(int32_t n, const int32_t *edges, int64_t m, int32_t flags,
+                          int32_t device, dm_graph **out);
+DM_API void dm_graph_destroy(dm_graph *g);
+DM_API int32_t dm_graph_num_vertices(const dm_graph *g);
+DM_API int64_t dm_graph_num_arcs(const dm_graph *g);  /* 2 |E_d| after dedup / self-loop removal */
+DM_API int32_t dm_graph_max_degree(const dm_graph *g);
+DM_API int32_t dm_graph_device(const dm_graph *g);
+/* Device pointers of the CSR (owned by g, valid until dm_graph_destroy). */
+DM_API dm_status dm_graph_device_csr(const dm_graph *g, const int64_t **d_off, const int32_t **d_adj);
+/* Copy the CSR to host buffers off_out[n+1] and adj_out[num_arcs] (either may be NULL). */
+DM_API dm_status dm_graph_copy_csr(const dm_graph *g, int64_t *off_out, int32_t *adj_out);
+
+/*
+ * dm_match -- all embeddings of the pattern (k vertices, pm edges p_edges[pm][2] on HOST) in
+ * g (Alg. 1).  opt may be NULL (defaults).
+ *   output & DM_OUT_COUNT: dm_result_count() = number of labelled mappings f (DESIGN Q2).
+ *   output & DM_OUT_TABLE: dm_result_rows() = host int32[count][k], row-major, column j =
+ *       f(j), rows in ascending lexicographic order.
+ * Only mappings with f(first plan vertex) in [seed_begin, seed_end) are produced, so disjoint
+ * seed ranges partition the result (multi-GPU sharding, DESIGN "Multi-GPU").  Use
+ * dm_plan_create + dm_plan_first_vertex to learn which pattern vertex that is.
+ * Errors: DM_ERR_ARG, DM_ERR_VERTEX_RANGE / DM_ERR_SELF_LOOP (pattern), DM_ERR_PATTERN_
+ * DISCONNECTED, DM_ERR_ROW_BUDGET (table mode only; count mode chunks instead), DM_ERR_OOM,
+ * DM_ERR_CUDA, DM_ERR_UNSUPPORTED (k > DM_MAX_PATTERN).
+ * The call is synchronous with respect to opt->cuda_stream (it reads back per-step sizes).
+ */
+DM_API dm_status dm_match(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                   const dm_match_opts *opt, dm_result **out);
+DM_API uint64_t dm_result_count(const dm_result *r);
+DM_API int32_t dm_result_width(const dm_result *r);          /* = k                                 */
+DM_API const int32_t *dm_result_rows(const dm_result *r);    /* host table or NULL (count only)     */
+DM_API dm_status dm_result_stats(const dm_result *r, dm_match_stats *out);
+DM_API void dm_result_free(dm_result *r);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+DM_API const char *dm_last_error(void);
+
+/*
+ * Host planner (no device needed).  dm_plan_create decomposes the pattern into motif slices
+ * exactly as §3.3 describes (motifs tried in descending size, first single match
+ * found by a backtracking matcher on the reduced pattern, boundary nodes kept, non-boundary
+ * nodes removed, shared vertices recorded as join constraints) and compiles the join program.
+ * motifs: DM_MOTIF_* bitmask (M2 always included); mode: DM_MONO / DM_INDUCED.
+ */
+DM_API dm_status dm_plan_create(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs,
+                         int32_t mode, dm_plan **out);
+DM_API void dm_plan_destroy(dm_plan *p);
+DM_API int32_t dm_plan_num_slices(const dm_plan *p);
+/* Slice i: motif id (DM_MOTIF_*), its pattern vertices (slot order, n_vertices <= 3) and the
+ * join constraints = vertices shared with the union of earlier slices. */
+DM_API dm_status dm_plan_slice(const dm_plan *p, int32_t i, int32_t *motif, int32_t *n_vertices,
+                        int32_t vertices[3], int32_t *n_constraints, int32_t constraints[3]);
+DM_API int32_t dm_plan_num_steps(const dm_plan *p);          /* executed kernel steps             */
+DM_API int32_t dm_plan_first_vertex(const dm_plan *p);       /* pattern vertex sharded by seed    */
+/* Human-readable JSON description of slices and steps (for tests / debugging).  Writes at
+ * most len bytes including the NUL; returns the full length needed. */
+DM_API int64_t dm_plan_describe(const dm_plan *p, char *buf, int64_t len);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DELTAMOTIF_H */

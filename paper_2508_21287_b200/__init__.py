@@ -1,0 +1,292 @@
+"""paper_2508_21287_b200 -- B200-native hot path of Delta-Motif (arXiv 2508.21287).
+
+Thin ctypes binding over ``libdeltamotif.so`` (C ABI declared in ``include/deltamotif.h``).
+This module only marshals arguments: graph construction, planning, every join step, the
+filters and the canonical sort all run inside the library (CUDA kernels for sm_100a plus the
+host planner).  There is no CPU fallback: if the library is missing or no CUDA device is
+present, the calls raise.
+
+    import paper_2508_21287_b200 as dm
+    g = dm.Graph(n, edges)                       # dm_graph_create  (device CSR, Res(M2))
+    r = g.match(k, pattern_edges, output="table")   # dm_match
+    r.count, r.rows, r.stats
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdeltamotif.so")
+
+DM_OK = 0
+ERRORS = {-1: "DM_ERR_ARG", -2: "DM_ERR_VERTEX_RANGE", -3: "DM_ERR_SELF_LOOP",
+          -4: "DM_ERR_PATTERN_DISCONNECTED", -5: "DM_ERR_OOM", -6: "DM_ERR_ROW_BUDGET",
+          -7: "DM_ERR_CUDA", -8: "DM_ERR_UNSUPPORTED"}
+DM_MONO, DM_INDUCED = 0, 1
+DM_OUT_COUNT, DM_OUT_TABLE = 1, 2
+DM_MOTIF_M2, DM_MOTIF_M3, DM_MOTIF_M3O = 1, 2, 4
+DM_GRAPH_DROP_SELF_LOOPS = 1
+DM_MATCH_PROFILE = 1
+DM_MAX_PATTERN = 64
+DM_MAX_STEPS = 64
+ABI_VERSION = 1
+
+MOTIF_SETS = {
+    "all": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O,
+    "M2": DM_MOTIF_M2,
+    "M3": DM_MOTIF_M2 | DM_MOTIF_M3,
+    "M3O": DM_MOTIF_M2 | DM_MOTIF_M3O,
+}
+
+
+class DMError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("mode", ctypes.c_int32), ("output", ctypes.c_int32), ("motifs", ctypes.c_int32),
+                ("flags", ctypes.c_int32), ("row_budget", ctypes.c_uint64),
+                ("mem_budget", ctypes.c_uint64), ("seed_begin", ctypes.c_int64),
+                ("seed_end", ctypes.c_int64), ("cuda_stream", ctypes.c_void_p)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("num_steps", ctypes.c_int32), ("num_launches", ctypes.c_int32),
+                ("num_chunks", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("rows_in", ctypes.c_uint64 * DM_MAX_STEPS),
+                ("rows_out", ctypes.c_uint64 * DM_MAX_STEPS),
+                ("candidates", ctypes.c_uint64 * DM_MAX_STEPS),
+                ("probes", ctypes.c_uint64 * DM_MAX_STEPS),
+                ("width_in", ctypes.c_int32 * DM_MAX_STEPS),
+                ("width_out", ctypes.c_int32 * DM_MAX_STEPS),
+                ("bytes_model", ctypes.c_double * DM_MAX_STEPS),
+                ("ms_count", ctypes.c_double * DM_MAX_STEPS),
+                ("ms_write", ctypes.c_double * DM_MAX_STEPS),
+                ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double)]
+
+
+_lib = None
+
+# every symbol include/deltamotif.h declares (checked by tests/test_abi.py)
+EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_destroy",
+           "dm_graph_num_vertices", "dm_graph_num_arcs", "dm_graph_max_degree",
+           "dm_graph_device", "dm_graph_device_csr", "dm_graph_copy_csr", "dm_match",
+           "dm_result_count", "dm_result_width", "dm_result_rows", "dm_result_stats",
+           "dm_result_free", "dm_last_error", "dm_plan_create", "dm_plan_destroy",
+           "dm_plan_num_slices", "dm_plan_slice", "dm_plan_num_steps", "dm_plan_first_vertex",
+           "dm_plan_describe"]
+
+
+def lib():
+    """Load libdeltamotif.so (raises loudly when it is missing: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (paper_2508_21287_b200 has no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    c = ctypes
+    P = c.c_void_p
+    sig = {
+        "dm_match_opts_init": (None, [c.POINTER(_Opts)]),
+        "dm_abi_version": (c.c_int32, []),
+        "dm_graph_create": (c.c_int, [c.c_int32, P, c.c_int64, c.c_int32, c.c_int32, c.POINTER(P)]),
+        "dm_graph_destroy": (None, [P]),
+        "dm_graph_num_vertices": (c.c_int32, [P]),
+        "dm_graph_num_arcs": (c.c_int64, [P]),
+        "dm_graph_max_degree": (c.c_int32, [P]),
+        "dm_graph_device": (c.c_int32, [P]),
+        "dm_graph_device_csr": (c.c_int, [P, c.POINTER(P), c.POINTER(P)]),
+        "dm_graph_copy_csr": (c.c_int, [P, P, P]),
+        "dm_match": (c.c_int, [P, c.c_int32, P, c.c_int64, c.POINTER(_Opts), c.POINTER(P)]),
+        "dm_result_count": (c.c_uint64, [P]),
+        "dm_result_width": (c.c_int32, [P]),
+        "dm_result_rows": (P, [P]),
+        "dm_result_stats": (c.c_int, [P, c.POINTER(_Stats)]),
+        "dm_result_free": (None, [P]),
+        "dm_last_error": (c.c_char_p, []),
+        "dm_plan_create": (c.c_int, [c.c_int32, P, c.c_int64, c.c_int32, c.c_int32, c.POINTER(P)]),
+        "dm_plan_destroy": (None, [P]),
+        "dm_plan_num_slices": (c.c_int32, [P]),
+        "dm_plan_slice": (c.c_int, [P, c.c_int32, c.POINTER(c.c_int32), c.POINTER(c.c_int32),
+                                    c.POINTER(c.c_int32), c.POINTER(c.c_int32),
+                                    c.POINTER(c.c_int32)]),
+        "dm_plan_num_steps": (c.c_int32, [P]),
+        "dm_plan_first_vertex": (c.c_int32, [P]),
+        "dm_plan_describe": (c.c_int64, [P, c.c_char_p, c.c_int64]),
+    }
+    for name, (rt, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = rt
+        f.argtypes = args
+    if L.dm_abi_version() != ABI_VERSION:
+        raise ImportError("libdeltamotif.so ABI version mismatch; rebuild")
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != DM_OK:
+        raise DMError(rc, (lib().dm_last_error() or b"").decode())
+
+
+def _edges_arr(edges) -> np.ndarray:
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+    return e
+
+
+def _motifs(m) -> int:
+    if isinstance(m, str):
+        return MOTIF_SETS[m]
+    return int(m)
+
+
+# ------------------------------------------------------------------------------- plans
+class Plan:
+    """Host join program (dm_plan_create): the §3.3 decomposition and the executed steps."""
+
+    def __init__(self, k: int, p_edges, motifs="all", mode: str = "mono"):
+        L = lib()
+        pe = _edges_arr(p_edges)
+        h = ctypes.c_void_p()
+        _check(L.dm_plan_create(k, pe.ctypes.data if pe.size else None, pe.shape[0], _motifs(motifs),
+                                DM_INDUCED if mode == "induced" else DM_MONO, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.dm_plan_destroy(self._h)
+            self._h = None
+
+    @property
+    def num_steps(self) -> int:
+        return lib().dm_plan_num_steps(self._h)
+
+    @property
+    def first_vertex(self) -> int:
+        return lib().dm_plan_first_vertex(self._h)
+
+    def slices(self):
+        L = lib()
+        out = []
+        names = {1: "M2", 2: "M3", 4: "M3-O"}
+        for i in range(L.dm_plan_num_slices(self._h)):
+            m, nv, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+            vs, cs = (ctypes.c_int32 * 3)(), (ctypes.c_int32 * 3)()
+            _check(L.dm_plan_slice(self._h, i, ctypes.byref(m), ctypes.byref(nv), vs, ctypes.byref(nc), cs))
+            out.append({"motif": names[m.value], "vertices": list(vs)[:nv.value],
+                        "constraints": list(cs)[:nc.value]})
+        return out
+
+    def describe(self) -> dict:
+        import json
+        L = lib()
+        n = L.dm_plan_describe(self._h, None, 0)
+        buf = ctypes.create_string_buffer(int(n))
+        L.dm_plan_describe(self._h, buf, n)
+        return json.loads(buf.value.decode())
+
+
+# ------------------------------------------------------------------------------ results
+class Result:
+    __slots__ = ("count", "rows", "stats")
+
+    def __init__(self, count, rows, stats):
+        self.count, self.rows, self.stats = count, rows, stats
+
+
+def _stats_dict(s: _Stats) -> dict:
+    n = s.num_steps
+    return {
+        "num_steps": n, "num_launches": s.num_launches, "num_chunks": s.num_chunks,
+        "rows_in": list(s.rows_in)[:n], "rows_out": list(s.rows_out)[:n],
+        "candidates": list(s.candidates)[:n], "probes": list(s.probes)[:n],
+        "width_in": list(s.width_in)[:n], "width_out": list(s.width_out)[:n],
+        "bytes_model": list(s.bytes_model)[:n], "ms_count": list(s.ms_count)[:n],
+        "ms_write": list(s.ms_write)[:n], "ms_other": s.ms_other, "ms_total": s.ms_total,
+    }
+
+
+# ------------------------------------------------------------------------------- graphs
+class Graph:
+    """Device-resident data graph (dm_graph_create): Res(M2) as a sorted CSR on `device`."""
+
+    def __init__(self, n: int, edges, *, drop_self_loops: bool = False, device: int = 0):
+        L = lib()
+        e = _edges_arr(edges)
+        h = ctypes.c_void_p()
+        _check(L.dm_graph_create(int(n), e.ctypes.data if e.size else None, e.shape[0],
+                                 DM_GRAPH_DROP_SELF_LOOPS if drop_self_loops else 0, int(device),
+                                 ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.dm_graph_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+    @property
+    def n(self) -> int:
+        return lib().dm_graph_num_vertices(self._h)
+
+    @property
+    def num_arcs(self) -> int:
+        return lib().dm_graph_num_arcs(self._h)
+
+    @property
+    def max_degree(self) -> int:
+        return lib().dm_graph_max_degree(self._h)
+
+    def csr(self):
+        """(off int64[n+1], adj int32[arcs]) copied to the host."""
+        off = np.zeros(self.n + 1, dtype=np.int64)
+        adj = np.zeros(max(self.num_arcs, 1), dtype=np.int32)
+        _check(lib().dm_graph_copy_csr(self._h, off.ctypes.data, adj.ctypes.data))
+        return off, adj[: self.num_arcs]
+
+    def match(self, k: int, p_edges, *, mode: str = "mono", output: str = "count",
+              motifs="all", seed_range=None, stream=None, profile: bool = False,
+              mem_budget: int = 0, row_budget: int = 0) -> Result:
+        """dm_match: embeddings of the pattern (k, p_edges).  output in {"count", "table",
+        "both"}; seed_range=(b, e) restricts f(first plan vertex) to [b, e); stream is a
+        torch.cuda.Stream / raw cudaStream_t int (None = legacy default stream)."""
+        L = lib()
+        pe = _edges_arr(p_edges)
+        o = _Opts()
+        L.dm_match_opts_init(ctypes.byref(o))
+        o.mode = DM_INDUCED if mode == "induced" else DM_MONO
+        o.output = {"count": DM_OUT_COUNT, "table": DM_OUT_TABLE, "both": DM_OUT_COUNT | DM_OUT_TABLE}[output]
+        o.motifs = _motifs(motifs)
+        o.flags = DM_MATCH_PROFILE if profile else 0
+        o.mem_budget = int(mem_budget)
+        o.row_budget = int(row_budget)
+        if seed_range is not None:
+            o.seed_begin, o.seed_end = int(seed_range[0]), int(seed_range[1])
+        if stream is not None:
+            o.cuda_stream = int(getattr(stream, "cuda_stream", stream))
+        r = ctypes.c_void_p()
+        _check(L.dm_match(self._h, int(k), pe.ctypes.data if pe.size else None, pe.shape[0],
+                          ctypes.byref(o), ctypes.byref(r)))
+        try:
+            cnt = int(L.dm_result_count(r))
+            rows = None
+            p = L.dm_result_rows(r)
+            if p and output in ("table", "both"):
+                buf = (ctypes.c_int32 * (cnt * k)).from_address(p)
+                rows = np.frombuffer(buf, dtype=np.int32).reshape(cnt, k).copy()
+            elif output in ("table", "both"):
+                rows = np.zeros((0, k), dtype=np.int32)
+            st = _Stats()
+            _check(L.dm_result_stats(r, ctypes.byref(st)))
+            return Result(cnt, rows, _stats_dict(st))
+        finally:
+            L.dm_result_free(r)

@@ -1,0 +1,79 @@
+// dm_device.cuh -- internal device-side declarations shared by the .cu files of
+// libdeltamotif.so (graph builder, join-step kernels, match driver).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "dm_internal.h"
+
+struct dm_graph {
+  int device = 0;
+  int32_t n = 0;
+  int64_t arcs = 0;     // 2|E| after dedup
+  int32_t max_deg = 0;
+  int64_t *d_off = nullptr;  // [n+1]
+  int32_t *d_adj = nullptr;  // [arcs], each list sorted ascending
+};
+
+namespace dm {
+
+#define DM_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t _e = (call);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return ::dm::fail(DM_ERR_CUDA, std::string(#call " failed: ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = false;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ------------------------------------------------------------- join-step kernel interface
+constexpr int kStepThreads = 256;   // threads per CTA
+constexpr int kTileRows = 256;      // frontier rows per CTA tile
+constexpr int kSurvBuf = 2048;      // survivors staged in shared memory per CTA
+
+// Device copy of one executed step (passed by value as a kernel parameter).
+struct DevStep {
+  int32_t in_w;
+  int32_t n_new;
+  int32_t n_nbr[2];
+  int32_t n_non[2];
+  uint8_t nbr[2][DM_MAX_PATTERN];
+  uint8_t non[2][DM_MAX_PATTERN];
+};
+
+struct StepIO {
+  const int32_t *in;          // [in_rows][in_w] row-major, or nullptr for the implicit seed
+  int64_t in_rows;            // rows of this launch's input (chunk)
+  int64_t seed_base;          // implicit seed: row r is vertex seed_base + r
+  int64_t block_begin;        // first tile index of this launch (chunked write passes)
+  int32_t *out;               // write pass: [*][in_w + n_new]
+  const uint64_t *block_off;  // write pass: exclusive prefix of survivors per tile (global)
+  uint64_t out_base;          // write pass: block_off value that maps to out row 0
+  uint64_t *block_cnt;        // count pass: survivors per tile (nullptr -> only total)
+  unsigned long long *total;  // count pass: += survivors (nullptr -> skip)
+  unsigned long long *stats;  // count pass: [0] += candidates, [1] += probes
+};
+
+size_t step_smem_bytes(int in_w, bool write_pass);
+cudaError_t launch_step_count(const DevStep &st, const StepIO &io, const dm_graph &g,
+                              int64_t num_tiles, cudaStream_t s);
+cudaError_t launch_step_write(const DevStep &st, const StepIO &io, const dm_graph &g,
+                              int64_t num_tiles, cudaStream_t s);
+
+DevStep make_dev_step(const Step &st);
+
+}  // namespace dm

@@ -1,0 +1,491 @@
+// match.cu -- dm_match: Alg. 1's join-and-filter loop driven on the host
+// over device-resident frontier tables, plus the canonical table output.
+//
+//   R := seed (the first slice's table, reading Q3 of DESIGN.md: R <- {} then InnerJoin means
+//        "R becomes the first slice's table"; here the seed is the first join step applied to
+//        the implicit one-column table of all data vertices in [seed_begin, seed_end))
+//   for each step: count pass -> exclusive scan of tile counts -> write pass (two-pass emit)
+//   last step in count mode: count pass only (the last level is never materialized)
+//
+// Frontier memory is bounded by chunking (depth-first across chunks, breadth-first inside a
+// chunk): when a level would exceed mem_budget bytes, its tiles are cut into groups whose
+// output fits (the count pass gives exact per-tile sizes) and each group is expanded to the
+// end before the next one is written.  Results do not depend on the chunking.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "dm_device.cuh"
+
+struct dm_result {
+  uint64_t count = 0;
+  int32_t k = 0;
+  int32_t *rows = nullptr;  // host, [count][k] canonical, or nullptr
+  dm_match_stats stats;
+};
+
+namespace dm {
+namespace {
+
+__global__ void k_iota(uint32_t *p, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = (uint32_t)i;
+}
+
+// keys[i] = table[perm[i]][col]
+__global__ void k_gather_col(const int32_t *__restrict__ table, int k, int col,
+                             const uint32_t *__restrict__ perm, uint32_t *__restrict__ keys,
+                             int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    keys[i] = (uint32_t)table[(int64_t)perm[i] * k + col];
+}
+
+// out[i][p] = table[perm[i]][pvert_col[p]]   (column permutation to pattern order)
+struct ColMap {
+  int32_t c[DM_MAX_PATTERN];
+};
+__global__ void k_gather_rows(const int32_t *__restrict__ table, int k, const ColMap cm,
+                              const uint32_t *__restrict__ perm, int32_t *__restrict__ out,
+                              int64_t n) {
+  const int64_t total = n * k;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i = t / k;
+    int p = (int)(t - i * k);
+    out[t] = table[(int64_t)perm[i] * k + cm.c[p]];
+  }
+}
+
+int grid_for(int64_t work) {
+  int64_t b = (work + 255) / 256;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
+}
+
+struct Prof {
+  bool on = false;
+  struct Ev {
+    cudaEvent_t a, b;
+    int step;
+    int kind;  // 0 count, 1 write, 2 other
+  };
+  std::vector<Ev> evs;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  cudaStream_t s = nullptr;
+  void begin(int step, int kind, Ev &e) {
+    if (!on) return;
+    e.step = step;
+    e.kind = kind;
+    cudaEventCreate(&e.a);
+    cudaEventCreate(&e.b);
+    cudaEventRecord(e.a, s);
+  }
+  void end(Ev &e) {
+    if (!on) return;
+    cudaEventRecord(e.b, s);
+    evs.push_back(e);
+  }
+  void finish(dm_match_stats &st) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    for (auto &e : evs) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e.a, e.b);
+      if (e.kind == 0) st.ms_count[e.step] += ms;
+      else if (e.kind == 1) st.ms_write[e.step] += ms;
+      else st.ms_other += ms;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    evs.clear();
+    if (t0 && t1) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, t0, t1);
+      st.ms_total = ms;
+    }
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+    t0 = t1 = nullptr;
+  }
+};
+
+struct Ctx {
+  const dm_graph *g = nullptr;
+  const Plan *plan = nullptr;
+  cudaStream_t s = nullptr;
+  bool table = false;
+  uint64_t mem_budget = 0;
+  uint64_t row_budget = 0;
+  std::vector<DevStep> dsteps;
+  unsigned long long *d_acc = nullptr;  // [0] count-mode total, [1+2i] C_i, [2+2i] Q_i
+  int32_t *d_res = nullptr;             // table mode: rows in column (match) order
+  uint64_t res_rows = 0, res_cap = 0;
+  dm_match_stats st;
+  Prof prof;
+};
+
+dm_status cuda_fail(cudaError_t e, const char *what) {
+  return fail(e == cudaErrorMemoryAllocation ? DM_ERR_OOM : DM_ERR_CUDA,
+              std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(call, what)                          \
+  do {                                          \
+    cudaError_t _e = (call);                    \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t alloc(size_t n, cudaStream_t st) {
+    s = st;
+    return cudaMallocAsync((void **)&p, sizeof(T) * std::max<size_t>(n, 1), st);
+  }
+  ~DevBuf() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+dm_status grow_result(Ctx &c, uint64_t need, int W) {
+  if (need <= c.res_cap) return DM_OK;
+  if (need > c.row_budget)
+    return fail(DM_ERR_ROW_BUDGET, "result table exceeds row_budget (" + std::to_string(need) +
+                                       " rows); use count mode or raise row_budget");
+  uint64_t cap = std::max<uint64_t>(need, c.res_cap * 2);
+  cap = std::min<uint64_t>(cap, std::max<uint64_t>(need, c.row_budget));
+  int32_t *p = nullptr;
+  CK(cudaMallocAsync((void **)&p, sizeof(int32_t) * (size_t)cap * W, c.s), "result allocation");
+  if (c.res_rows)
+    CK(cudaMemcpyAsync(p, c.d_res, sizeof(int32_t) * (size_t)c.res_rows * W,
+                       cudaMemcpyDeviceToDevice, c.s),
+       "result copy");
+  if (c.d_res) cudaFreeAsync(c.d_res, c.s);
+  c.d_res = p;
+  c.res_cap = cap;
+  return DM_OK;
+}
+
+dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t seed_base) {
+  if (in_rows <= 0) return DM_OK;
+  const int nsteps = (int)c.plan->steps.size();
+  const DevStep &D = c.dsteps[(size_t)si];
+  const bool last = si == nsteps - 1;
+  const int W = D.in_w + D.n_new;
+  const int64_t tiles = (in_rows + kTileRows - 1) / kTileRows;
+  c.st.rows_in[si] += (uint64_t)in_rows;
+  c.st.num_chunks++;
+
+  StepIO io{};
+  io.in = in;
+  io.in_rows = in_rows;
+  io.seed_base = seed_base;
+  io.block_begin = 0;
+  io.stats = c.d_acc + 1 + 2 * si;
+
+  if (last && !c.table) {  // count-only last step: reduce, never materialize
+    io.total = c.d_acc;
+    Prof::Ev e;
+    c.prof.begin(si, 0, e);
+    CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
+    c.prof.end(e);
+    c.st.num_launches++;
+    return DM_OK;
+  }
+
+  DevBuf<uint64_t> cnt, scan;
+  CK(cnt.alloc((size_t)tiles + 1, c.s), "tile counts");
+  CK(scan.alloc((size_t)tiles + 1, c.s), "tile scan");
+  io.block_cnt = cnt.p;
+  {
+    Prof::Ev e;
+    c.prof.begin(si, 0, e);
+    CK(cudaMemsetAsync(cnt.p + tiles, 0, sizeof(uint64_t), c.s), "memset");
+    CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
+    c.prof.end(e);
+    c.st.num_launches++;
+  }
+  {
+    Prof::Ev e;
+    c.prof.begin(si, 2, e);
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, scan.p, tiles + 1, c.s), "scan");
+    DevBuf<unsigned char> tmp;
+    CK(tmp.alloc(tb, c.s), "scan temp");
+    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, scan.p, tiles + 1, c.s), "scan");
+    c.prof.end(e);
+    c.st.num_launches++;
+  }
+  uint64_t total = 0;
+  CK(cudaMemcpyAsync(&total, scan.p + tiles, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s), "D2H");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  c.st.rows_out[si] += total;
+  if (total == 0) return DM_OK;
+  io.block_cnt = nullptr;
+  io.stats = nullptr;
+  io.block_off = scan.p;
+
+  if (last) {  // table mode: append to the result table
+    dm_status stt = grow_result(c, c.res_rows + total, W);
+    if (stt != DM_OK) return stt;
+    io.out = c.d_res + (size_t)c.res_rows * W;
+    io.out_base = 0;
+    Prof::Ev e;
+    c.prof.begin(si, 1, e);
+    CK(launch_step_write(D, io, *c.g, tiles, c.s), "write kernel");
+    c.prof.end(e);
+    c.st.num_launches++;
+    c.res_rows += total;
+    return DM_OK;
+  }
+
+  const uint64_t row_bytes = (uint64_t)W * sizeof(int32_t);
+  if (total * row_bytes <= c.mem_budget) {
+    DevBuf<int32_t> out;
+    CK(out.alloc((size_t)total * W, c.s), "frontier allocation");
+    io.out = out.p;
+    io.out_base = 0;
+    Prof::Ev e;
+    c.prof.begin(si, 1, e);
+    CK(launch_step_write(D, io, *c.g, tiles, c.s), "write kernel");
+    c.prof.end(e);
+    c.st.num_launches++;
+    return run_step(c, si + 1, out.p, (int64_t)total, 0);
+  }
+  // chunked: groups of tiles whose output fits the budget
+  std::vector<uint64_t> h((size_t)tiles + 1);
+  CK(cudaMemcpyAsync(h.data(), scan.p, sizeof(uint64_t) * ((size_t)tiles + 1),
+                     cudaMemcpyDeviceToHost, c.s),
+     "D2H scan");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  const uint64_t budget_rows = std::max<uint64_t>(1, c.mem_budget / row_bytes);
+  int64_t b0 = 0;
+  while (b0 < tiles) {
+    int64_t b1 = b0 + 1;
+    while (b1 < tiles && h[(size_t)b1 + 1] - h[(size_t)b0] <= budget_rows) ++b1;
+    const uint64_t rows = h[(size_t)b1] - h[(size_t)b0];
+    if (rows > 0) {
+      DevBuf<int32_t> out;
+      CK(out.alloc((size_t)rows * W, c.s), "frontier chunk allocation");
+      io.out = out.p;
+      io.out_base = h[(size_t)b0];
+      io.block_begin = b0;
+      Prof::Ev e;
+      c.prof.begin(si, 1, e);
+      CK(launch_step_write(D, io, *c.g, b1 - b0, c.s), "write kernel");
+      c.prof.end(e);
+      c.st.num_launches++;
+      dm_status stt = run_step(c, si + 1, out.p, (int64_t)rows, 0);
+      if (stt != DM_OK) return stt;
+    }
+    b0 = b1;
+  }
+  return DM_OK;
+}
+
+// Permute columns to pattern order and sort rows lexicographically (LSD radix sort over the
+// columns, last column first).  Writes host rows.
+dm_status canonicalize(Ctx &c, int32_t *host_out) {
+  const int k = c.plan->k;
+  const int64_t n = (int64_t)c.res_rows;
+  if (n == 0) return DM_OK;
+  if (n >= (int64_t)UINT32_MAX) return fail(DM_ERR_ROW_BUDGET, "table too large to sort");
+  int end_bit = 1;
+  while (end_bit < 32 && ((uint64_t)c.g->n >> end_bit) != 0) ++end_bit;
+  DevBuf<uint32_t> keys, keys2, perm, perm2;
+  CK(keys.alloc((size_t)n, c.s), "sort keys");
+  CK(keys2.alloc((size_t)n, c.s), "sort keys");
+  CK(perm.alloc((size_t)n, c.s), "sort perm");
+  CK(perm2.alloc((size_t)n, c.s), "sort perm");
+  Prof::Ev e;
+  c.prof.begin(0, 2, e);
+  k_iota<<<grid_for(n), 256, 0, c.s>>>(perm.p, n);
+  CK(cudaGetLastError(), "iota");
+  c.st.num_launches++;
+  cub::DoubleBuffer<uint32_t> dk(keys.p, keys2.p), dv(perm.p, perm2.p);
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n, 0, end_bit, c.s), "sort");
+  DevBuf<unsigned char> tmp;
+  CK(tmp.alloc(tb, c.s), "sort temp");
+  for (int p = k - 1; p >= 0; --p) {
+    const int col = c.plan->pvert_col[(size_t)p];
+    k_gather_col<<<grid_for(n), 256, 0, c.s>>>(c.d_res, k, col, dv.Current(), dk.Current(), n);
+    CK(cudaGetLastError(), "gather");
+    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, n, 0, end_bit, c.s), "sort");
+    c.st.num_launches += 2;
+  }
+  ColMap cm{};
+  for (int p = 0; p < k; ++p) cm.c[p] = c.plan->pvert_col[(size_t)p];
+  DevBuf<int32_t> outb;
+  CK(outb.alloc((size_t)n * k, c.s), "canonical table");
+  k_gather_rows<<<grid_for(n * k), 256, 0, c.s>>>(c.d_res, k, cm, dv.Current(), outb.p, n);
+  CK(cudaGetLastError(), "gather rows");
+  c.st.num_launches++;
+  c.prof.end(e);
+  CK(cudaMemcpyAsync(host_out, outb.p, sizeof(int32_t) * (size_t)n * k, cudaMemcpyDeviceToHost, c.s),
+     "D2H table");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  return DM_OK;
+}
+
+void configure_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
+dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                     const dm_match_opts *opt_in, dm_result **out) {
+  if (!g || !out) return fail(DM_ERR_ARG, "graph/out is NULL");
+  dm_match_opts opt;
+  dm_match_opts_init(&opt);
+  if (opt_in) opt = *opt_in;
+  if (!(opt.output & (DM_OUT_COUNT | DM_OUT_TABLE))) return fail(DM_ERR_ARG, "output must request count and/or table");
+  Plan plan;
+  dm_status stt = build_plan(k, p_edges, pm, opt.motifs, opt.mode, plan);
+  if (stt != DM_OK) return stt;
+  int64_t sb = std::max<int64_t>(0, opt.seed_begin);
+  int64_t se = opt.seed_end < 0 ? g->n : std::min<int64_t>(opt.seed_end, g->n);
+  if (se < sb) se = sb;
+
+  DeviceGuard dgd(g->device);
+  if (!dgd.ok) return fail(DM_ERR_CUDA, "cudaSetDevice failed");
+  configure_pool(g->device);
+
+  Ctx c;
+  c.g = g;
+  c.plan = &plan;
+  c.s = (cudaStream_t)opt.cuda_stream;
+  c.table = (opt.output & DM_OUT_TABLE) != 0;
+  c.row_budget = opt.row_budget ? opt.row_budget : (1ull << 27);
+  std::memset(&c.st, 0, sizeof(c.st));
+  c.st.num_steps = (int32_t)plan.steps.size();
+  for (auto &s : plan.steps) c.dsteps.push_back(make_dev_step(s));
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    c.st.width_in[i] = plan.steps[i].in_w;
+    c.st.width_out[i] = plan.steps[i].in_w + plan.steps[i].n_new;
+  }
+  if (opt.mem_budget) {
+    c.mem_budget = opt.mem_budget;
+  } else {
+    size_t fr = 0, tot = 0;
+    CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    uint64_t per = (uint64_t)(fr * 0.7) / (uint64_t)(plan.steps.size() + 2);
+    c.mem_budget = std::max<uint64_t>(per, 64ull << 20);
+  }
+  c.prof.on = (opt.flags & DM_MATCH_PROFILE) != 0;
+  c.prof.s = c.s;
+
+  dm_result *res = new (std::nothrow) dm_result;
+  if (!res) return fail(DM_ERR_OOM, "host allocation failed");
+  res->k = k;
+  struct ResGuard {
+    dm_result *&r;
+    bool keep = false;
+    ~ResGuard() {
+      if (!keep) {
+        if (r) std::free(r->rows);
+        delete r;
+      }
+    }
+  } rg{res};
+
+  const int nacc = 1 + 2 * (int)plan.steps.size();
+  CK(cudaMallocAsync((void **)&c.d_acc, sizeof(unsigned long long) * nacc, c.s), "accumulators");
+  struct AccGuard {
+    Ctx &c;
+    ~AccGuard() {
+      if (c.d_acc) cudaFreeAsync(c.d_acc, c.s);
+      if (c.d_res) cudaFreeAsync(c.d_res, c.s);
+    }
+  } ag{c};
+  CK(cudaMemsetAsync(c.d_acc, 0, sizeof(unsigned long long) * nacc, c.s), "memset");
+  if (c.prof.on) {
+    cudaEventCreate(&c.prof.t0);
+    cudaEventCreate(&c.prof.t1);
+    cudaEventRecord(c.prof.t0, c.s);
+  }
+
+  uint64_t count = 0;
+  if (plan.steps.empty()) {  // k == 1: every data vertex of the shard (Q7)
+    count = (uint64_t)(se - sb);
+    if (c.table) {
+      if (count > c.row_budget) return fail(DM_ERR_ROW_BUDGET, "result table exceeds row_budget");
+      res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count, 1));
+      if (!res->rows) return fail(DM_ERR_OOM, "host allocation failed");
+      for (uint64_t i = 0; i < count; ++i) res->rows[i] = (int32_t)(sb + (int64_t)i);
+    }
+  } else {
+    stt = run_step(c, 0, nullptr, se - sb, sb);
+    if (stt != DM_OK) return stt;
+    if (c.table) {
+      count = c.res_rows;
+      res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count * k, 1));
+      if (!res->rows) return fail(DM_ERR_OOM, "host allocation failed");
+      stt = canonicalize(c, res->rows);
+      if (stt != DM_OK) return stt;
+    }
+  }
+  if (c.prof.on) cudaEventRecord(c.prof.t1, c.s);
+  std::vector<unsigned long long> acc((size_t)nacc);
+  CK(cudaMemcpyAsync(acc.data(), c.d_acc, sizeof(unsigned long long) * nacc, cudaMemcpyDeviceToHost, c.s),
+     "D2H accumulators");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  if (!plan.steps.empty() && !c.table) count = acc[0];
+  if (!plan.steps.empty() && !c.table) c.st.rows_out[plan.steps.size() - 1] = count;
+  c.prof.finish(c.st);
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    c.st.candidates[i] = acc[1 + 2 * i];
+    c.st.probes[i] = acc[2 + 2 * i];
+    const bool lastc = (i + 1 == plan.steps.size()) && !c.table;
+    const double win = (i == 0) ? 0.0 : (double)c.st.width_in[i];  // the seed input is implicit
+    c.st.bytes_model[i] = 4.0 * win * (double)c.st.rows_in[i] + 8.0 * (double)c.st.rows_in[i] +
+                          4.0 * (double)c.st.candidates[i] + 4.0 * (double)c.st.probes[i] +
+                          (lastc ? 0.0 : 4.0 * c.st.width_out[i] * (double)c.st.rows_out[i]);
+  }
+  res->count = count;
+  res->stats = c.st;
+  rg.keep = true;
+  *out = res;
+  return DM_OK;
+}
+
+}  // namespace
+}  // namespace dm
+
+extern "C" {
+
+dm_status dm_match(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                   const dm_match_opts *opt, dm_result **out) {
+  dm::clear_error();
+  return dm::match_impl(g, k, p_edges, pm, opt, out);
+}
+
+uint64_t dm_result_count(const dm_result *r) { return r ? r->count : 0; }
+int32_t dm_result_width(const dm_result *r) { return r ? r->k : -1; }
+const int32_t *dm_result_rows(const dm_result *r) { return r ? r->rows : nullptr; }
+
+dm_status dm_result_stats(const dm_result *r, dm_match_stats *out) {
+  dm::clear_error();
+  if (!r || !out) return dm::fail(DM_ERR_ARG, "NULL argument");
+  *out = r->stats;
+  return DM_OK;
+}
+
+void dm_result_free(dm_result *r) {
+  if (!r) return;
+  std::free(r->rows);
+  delete r;
+}
+
+}  // extern "C"
