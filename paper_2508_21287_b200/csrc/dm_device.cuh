@@ -43,7 +43,10 @@ struct DeviceGuard {
 // ------------------------------------------------------------- join-step kernel interface
 constexpr int kStepThreads = 256;   // threads per CTA
 constexpr int kTileRows = 256;      // frontier rows per CTA tile
-constexpr int kSurvBuf = 2048;      // survivors staged in shared memory per CTA
+constexpr int kSurvBuf = 1024;      // survivors staged in shared memory per CTA
+constexpr int kModeCount = 0;       // join-step kernel launch modes (see extend.cu)
+constexpr int kModeWrite = 1;
+constexpr int kModeSingle = 2;
 
 // Device copy of one executed step (passed by value as a kernel parameter).
 struct DevStep {
@@ -65,7 +68,11 @@ struct StepIO {
   uint64_t out_base;          // write pass: block_off value that maps to out row 0
   uint64_t *block_cnt;        // count pass: survivors per tile (nullptr -> only total)
   unsigned long long *total;  // count pass: += survivors (nullptr -> skip)
-  unsigned long long *stats;  // count pass: [0] += candidates, [1] += probes
+  unsigned long long *stats;  // [0] += candidates, [1] += probes (nullptr -> skip)
+  unsigned long long *status; // single pass: look-back status word per tile (zeroed)
+  unsigned long long *ctrl;   // single pass: [0] tile counter (0), [1] first unwritten tile
+                              //   (init = #tiles), [2] += survivors
+  uint64_t cap;               // single pass: output capacity in rows
 };
 
 size_t step_smem_bytes(int in_w, bool write_pass);
@@ -73,6 +80,10 @@ cudaError_t launch_step_count(const DevStep &st, const StepIO &io, const dm_grap
                               int64_t num_tiles, cudaStream_t s);
 cudaError_t launch_step_write(const DevStep &st, const StepIO &io, const dm_graph &g,
                               int64_t num_tiles, cudaStream_t s);
+cudaError_t launch_step_single(const DevStep &st, const StepIO &io, const dm_graph &g,
+                               int64_t num_tiles, cudaStream_t s);
+cudaError_t launch_status_to_excl(const unsigned long long *status, int64_t tiles, uint64_t *excl,
+                                  cudaStream_t s);
 
 DevStep make_dev_step(const Step &st);
 

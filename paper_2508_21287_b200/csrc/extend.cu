@@ -1,29 +1,34 @@
-// extend.cu -- the join step of Alg. 1 as one fused sm_100a kernel,
-// launched twice per materialized step (count pass, write pass):
+// extend.cu -- the join step of Alg. 1 as one fused sm_100a kernel:
 //
 //   R <- InnerJoin(R, Res(M), C)        (equi-join on the key columns)
 //   R <- FilterOverlappingNodes(R)      (all-distinct rule, P:237 / S:213)
 //
 // Res(M2) is the device CSR (sorted, both orientations), so the equi-join of a frontier row
-// with Res(M2) on one key column is the CSR range of that key ("sort-merge join" with the
+// with Res(M2) on one key column is the CSR range of that key (a sort-merge join against the
 // sorted edge table), and every further join key is a lookup of (key, candidate) in the
-// sorted edge table (a 2-key equi-join with Res(M2), i.e. the closing-edge probe of Fig. 2
-// C1/C2).  Per frontier row and new pattern vertex, the key column whose data vertex has the
-// smallest degree supplies the candidates (iterating the smaller side of the join); the
-// other keys are probed by binary search in the shorter of the two adjacency lists.
+// sorted edge table (a 2-key equi-join with Res(M2): the closing-edge probe of Fig. 2 C1/C2).
+// Per frontier row and new pattern vertex, the key column whose data vertex has the smallest
+// degree supplies the candidates (iterating the smaller side of the join); the other keys are
+// probed by binary search in the shorter of the two adjacency lists.
 //
 // CTA = one tile of kTileRows consecutive frontier rows (one contiguous block of memory):
-//   1. coalesced 16-byte loads of the tile into shared memory;
-//   2. per row: choose the key (anchor) for the first new vertex, candidate count = degree;
-//      CTA exclusive scan -> the tile's candidate space (load-balanced across the CTA even
-//      when one row owns a hub);
-//   3. each thread takes candidates j, tid + j*NT: injectivity against the row (FilterOverlapping-
-//      Nodes) + closing-edge probes (+ non-edge probes in induced mode); for 2-vertex steps
-//      (wedge / triangle slices) the second new vertex is enumerated the same way;
-//   4. count pass: CTA sum -> block_cnt[tile] (and the running total / statistics);
-//      write pass: CTA scan of survivors -> survivor list staged in shared memory -> warp-
-//      cooperative coalesced row writes at the tile's offset from the exclusive scan of the
-//      count pass.  Output order is deterministic (row order, then candidate order).
+//   1. tile -> shared memory with one TMA bulk copy (cp.async.bulk + mbarrier);
+//   2. per row: join key (anchor) of the first new vertex, candidate count = its degree; CTA
+//      exclusive scan -> the tile's candidate space (a hub row is spread over the CTA);
+//   3. rounds of kStepThreads candidates: injectivity + closing-edge (+ induced non-edge)
+//      probes; for 2-vertex steps (wedge / triangle slices) the accepted first vertices of the
+//      round and their second-vertex candidate counts are scanned again, so every second-level
+//      candidate is one thread too (each candidate is evaluated exactly once per launch);
+//   4. survivors are staged in shared memory (CTA scan -> deterministic order: row order, then
+//      candidate order) and written with warp-cooperative coalesced row stores.
+//
+// Launch modes:
+//   kModeCount  : count only (the count-mode last step: the last level is never materialized);
+//   kModeWrite  : write at offsets from an exclusive prefix over tiles (re-run / chunked path);
+//   kModeSingle : single pass with decoupled look-back -- each tile publishes its survivor
+//                 count, looks back for its exclusive prefix and writes immediately if the
+//                 output capacity allows; tiles that do not fit (capacity or staging buffer)
+//                 record themselves and are re-run by the host with kModeWrite.
 #include <cub/cub.cuh>
 
 #include <mutex>
@@ -33,6 +38,10 @@
 namespace dm {
 
 namespace {
+
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPrefix = 2ull << 62;
+constexpr unsigned long long kValueMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ int64_t degree(const int64_t *__restrict__ off, int32_t v) {
   return __ldg(off + v + 1) - __ldg(off + v);
@@ -58,31 +67,72 @@ __device__ __forceinline__ bool has_edge(const int64_t *__restrict__ off,
   return lo < end && __ldg(adj + lo) == key;
 }
 
+// x in row?  branch-free, unrolled by 4 (rows sit at stride w in shared memory; for odd w a
+// warp's rows fall in distinct banks).
+__device__ __forceinline__ bool in_row(const int32_t *row, int w, int32_t x) {
+  bool hit = false;
+  int c = 0;
+  for (; c + 4 <= w; c += 4) {
+    const int32_t a = row[c], b = row[c + 1], d = row[c + 2], e = row[c + 3];
+    hit |= (a == x) | (b == x) | (d == x) | (e == x);
+  }
+  for (; c < w; ++c) hit |= row[c] == x;
+  return hit;
+}
+
+// ---- TMA 1-D bulk copy global -> shared, completion tracked by an mbarrier (sm_90+ / sm_100a)
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+      "l"(src), "r"(bytes), "r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(phase)
+        : "memory");
+  }
+}
+
 // value of column c of the row being built (c == w -> first new vertex)
 __device__ __forceinline__ int32_t colval(const int32_t *row, int w, int c, int32_t x0) {
   return c < w ? row[c] : x0;
 }
 
-// Filters for new vertex j with candidate value x (anchor column `acol` already satisfied):
-// all-distinct, closing-edge probes, induced non-edge probes.
-template <bool STATS>
+// Filters for new vertex j with candidate value x (anchor column `acol` is satisfied by
+// construction): all-distinct, closing-edge probes, induced non-edge probes.
 __device__ __forceinline__ bool accept(const DevStep &st, int j, const int32_t *row, int w,
                                        int32_t x0, int32_t x, int acol,
                                        const int64_t *__restrict__ off,
-                                       const int32_t *__restrict__ adj, uint64_t &probes) {
-  for (int c = 0; c < w; ++c)
-    if (row[c] == x) return false;
+                                       const int32_t *__restrict__ adj, uint32_t &probes) {
+  if (in_row(row, w, x)) return false;
   if (j == 1 && x == x0) return false;
   for (int t = 0; t < st.n_nbr[j]; ++t) {
     int c = st.nbr[j][t];
     if (c == acol) continue;
-    if (STATS) ++probes;
+    ++probes;
     if (!has_edge(off, adj, colval(row, w, c, x0), x)) return false;
   }
   for (int t = 0; t < st.n_non[j]; ++t) {
-    int c = st.non[j][t];
-    if (STATS) ++probes;
-    if (has_edge(off, adj, colval(row, w, c, x0), x)) return false;
+    ++probes;
+    if (has_edge(off, adj, colval(row, w, st.non[j][t], x0), x)) return false;
   }
   return true;
 }
@@ -107,40 +157,52 @@ __device__ __forceinline__ int pick_anchor(const DevStep &st, int j, const int32
   return best;
 }
 
-struct SmemLayout {
-  int32_t *rows;
-  long long *pref;
-  int32_t *anc;
-  int32_t *acol;
-  int32_t *sv_row;
-  int32_t *sv_x;
-};
-
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline size_t smem_bytes(int in_w, bool write) {
+struct SmemLayout {
+  int32_t *rows;     // [kTileRows][w] (the tile, contiguous as in global memory)
+  long long *pref;   // [kTileRows]    first-vertex candidate prefix
+  int32_t *anc;      // [kTileRows]    first-vertex anchor vertex
+  int32_t *acol;     // [kTileRows]    first-vertex anchor column
+  long long *apref;  // [kStepThreads] second-vertex candidate prefix (per round)
+  int32_t *ar;       // [kStepThreads] row of the accepted first vertex
+  int32_t *ax0;      // [kStepThreads] accepted first vertex
+  int32_t *aav;      // [kStepThreads] second-vertex anchor vertex
+  int32_t *aacol;    // [kStepThreads] second-vertex anchor column
+  int32_t *sv_row;   // [kSurvBuf]
+  int32_t *sv_x;     // [kSurvBuf][2]
+};
+
+__host__ __device__ inline size_t smem_bytes(int in_w, bool stage) {
   size_t b = align16(sizeof(int32_t) * (size_t)kTileRows * in_w);
-  b += align16(sizeof(long long) * (kTileRows + 1));
-  b += align16(sizeof(int32_t) * kTileRows) * 2;
-  if (write) b += align16(sizeof(int32_t) * kSurvBuf) + align16(sizeof(int32_t) * 2 * kSurvBuf);
+  b += align16(sizeof(long long) * kTileRows);
+  b += 2 * align16(sizeof(int32_t) * kTileRows);
+  b += align16(sizeof(long long) * kStepThreads);
+  b += 4 * align16(sizeof(int32_t) * kStepThreads);
+  if (stage) b += align16(sizeof(int32_t) * kSurvBuf) + align16(sizeof(int32_t) * 2 * kSurvBuf);
   return b;
 }
 
-__device__ inline SmemLayout carve(unsigned char *base, int in_w, bool write) {
+__device__ inline SmemLayout carve(unsigned char *base, int in_w, bool stage) {
   SmemLayout L;
   size_t o = 0;
-  L.rows = reinterpret_cast<int32_t *>(base + o);
-  o += align16(sizeof(int32_t) * (size_t)kTileRows * in_w);
-  L.pref = reinterpret_cast<long long *>(base + o);
-  o += align16(sizeof(long long) * (kTileRows + 1));
-  L.anc = reinterpret_cast<int32_t *>(base + o);
-  o += align16(sizeof(int32_t) * kTileRows);
-  L.acol = reinterpret_cast<int32_t *>(base + o);
-  o += align16(sizeof(int32_t) * kTileRows);
-  if (write) {
-    L.sv_row = reinterpret_cast<int32_t *>(base + o);
-    o += align16(sizeof(int32_t) * kSurvBuf);
-    L.sv_x = reinterpret_cast<int32_t *>(base + o);
+  auto take = [&](size_t bytes) {
+    unsigned char *p = base + o;
+    o += align16(bytes);
+    return p;
+  };
+  L.rows = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * (size_t)kTileRows * in_w));
+  L.pref = reinterpret_cast<long long *>(take(sizeof(long long) * kTileRows));
+  L.anc = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kTileRows));
+  L.acol = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kTileRows));
+  L.apref = reinterpret_cast<long long *>(take(sizeof(long long) * kStepThreads));
+  L.ar = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
+  L.ax0 = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
+  L.aav = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
+  L.aacol = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
+  if (stage) {
+    L.sv_row = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kSurvBuf));
+    L.sv_x = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * 2 * kSurvBuf));
   } else {
     L.sv_row = L.sv_x = nullptr;
   }
@@ -171,7 +233,14 @@ __device__ __forceinline__ void flush_rows(const SmemLayout &L, int w, int W, in
   }
 }
 
-template <bool WRITE>
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+  return *reinterpret_cast<const volatile unsigned long long *>(p);
+}
+__device__ __forceinline__ void st_volatile(unsigned long long *p, unsigned long long v) {
+  *reinterpret_cast<volatile unsigned long long *>(p) = v;
+}
+
+template <int MODE>
 __global__ void __launch_bounds__(kStepThreads)
     k_step(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
@@ -184,28 +253,47 @@ __global__ void __launch_bounds__(kStepThreads)
     typename ScanI::TempStorage i;
     typename RedU::TempStorage r;
   } tmp;
+  __shared__ unsigned long long s_bc;
+  __shared__ __align__(8) uint64_t s_bar;
+  constexpr bool kStage = MODE != kModeCount;
 
   const int w = st.in_w;
   const int W = w + st.n_new;
   const int tid = threadIdx.x;
-  const int64_t tile = io.block_begin + blockIdx.x;
+  int64_t tile;
+  if (MODE == kModeSingle) {
+    if (tid == 0) s_bc = atomicAdd(io.ctrl + 0, 1ull);  // dynamic tile id: forward progress
+    __syncthreads();
+    tile = (int64_t)s_bc;
+  } else {
+    tile = io.block_begin + blockIdx.x;
+  }
   const int64_t r0 = tile * kTileRows;
   if (r0 >= io.in_rows) return;
   const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
-  SmemLayout L = carve(smem_raw, w, WRITE);
+  SmemLayout L = carve(smem_raw, w, kStage);
 
-  // ---- 1. tile -> shared memory (contiguous rows; 16-byte vector loads)
+  // ---- 1. tile -> shared memory: one TMA bulk copy of the contiguous tile (16-byte multiple;
+  //         the <= 3-word tail of the last tile with plain loads), mbarrier completion
   if (io.in) {
     const int32_t *src = io.in + r0 * w;
     const int nw = nrows * w;
-    const int n4 = nw >> 2;
-    const int4 *src4 = reinterpret_cast<const int4 *>(src);  // r0*w % 4 == 0 (kTileRows % 4 == 0)
-    int4 *dst4 = reinterpret_cast<int4 *>(L.rows);
-#pragma unroll 4
-    for (int i = tid; i < n4; i += kStepThreads) dst4[i] = __ldcs(src4 + i);
-    for (int i = (n4 << 2) + tid; i < nw; i += kStepThreads) L.rows[i] = __ldcs(src + i);
+    const unsigned bulk = (unsigned)(nw & ~3) * 4u;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
+    if (aligned && bulk > 0) {
+      if (tid == 0) mbar_init(&s_bar, 1);
+      __syncthreads();
+      if (tid == 0) {
+        mbar_expect_tx(&s_bar, bulk);
+        tma_bulk_g2s(L.rows, src, bulk, &s_bar);
+      }
+      for (int i = (nw & ~3) + tid; i < nw; i += kStepThreads) L.rows[i] = __ldcs(src + i);
+      mbar_wait(&s_bar, 0);
+    } else {
+      for (int i = tid; i < nw; i += kStepThreads) L.rows[i] = __ldcs(src + i);
+    }
   } else {
-    for (int i = tid; i < nrows; i += kStepThreads) L.rows[i] = (int32_t)(io.seed_base + r0 + i);
+    for (int r = tid; r < nrows; r += kStepThreads) L.rows[r] = (int32_t)(io.seed_base + r0 + r);
   }
   __syncthreads();
 
@@ -218,22 +306,55 @@ __global__ void __launch_bounds__(kStepThreads)
     L.anc[tid] = av;
     cnt = ad;
   }
-  long long pref, C;
-  ScanLL(tmp.ll).ExclusiveSum(cnt, pref, C);
+  long long pref, C0;
+  ScanLL(tmp.ll).ExclusiveSum(cnt, pref, C0);
   L.pref[tid] = pref;
   __syncthreads();
 
-  // ---- 3. candidates
-  uint64_t my_surv = 0, my_cand = 0, my_probe = 0;
-  int fill = 0;            // staged survivors (WRITE)
-  int64_t base = 0;        // next output row (WRITE)
-  if (WRITE) base = (int64_t)(io.block_off[tile] - io.out_base);
+  uint32_t my_cand = 0, my_probe = 0;
+  unsigned long long my_surv = 0;  // kModeCount
+  int fill = 0;                    // staged survivors
+  long long agg = 0;               // kModeSingle: survivors of the tile
+  bool ovf = false;                // kModeSingle: staging buffer overflowed
+  int64_t base = 0;                // kModeWrite: next output row
+  if (MODE == kModeWrite) base = (int64_t)(io.block_off[tile] - io.out_base);
 
-  for (long long j0 = 0; j0 < C; j0 += kStepThreads) {
+  // block-wide: at most one survivor per thread
+  auto emit = [&](bool s, int r, int32_t x0, int32_t x1) {
+    if (MODE == kModeCount) {
+      my_surv += s;
+      return;
+    }
+    int pos, tot;
+    ScanI(tmp.i).ExclusiveSum(s ? 1 : 0, pos, tot);
+    if (MODE == kModeWrite && fill + tot > kSurvBuf) {
+      __syncthreads();
+      flush_rows(L, w, W, fill, io.out, base);
+      __syncthreads();
+      base += fill;
+      fill = 0;
+    }
+    if (MODE == kModeSingle) {
+      agg += tot;
+      if (fill + tot > kSurvBuf) ovf = true;
+    }
+    if (s && !ovf) {
+      const int p = fill + pos;
+      L.sv_row[p] = r;
+      L.sv_x[2 * p] = x0;
+      L.sv_x[2 * p + 1] = x1;
+    }
+    if (!ovf) fill += tot;
+    __syncthreads();  // scan storage reuse
+  };
+
+  // ---- 3. candidate rounds
+  for (long long j0 = 0; j0 < C0; j0 += kStepThreads) {
     const long long j = j0 + tid;
-    int r = -1, ns = 0;
+    int r = 0;
     int32_t x0 = -1;
-    if (j < C) {
+    bool ok = false;
+    if (j < C0) {
       int lo = 0, hi = nrows;  // largest r with pref[r] <= j
       while (hi - lo > 1) {
         int mid = (lo + hi) >> 1;
@@ -241,126 +362,114 @@ __global__ void __launch_bounds__(kStepThreads)
         else hi = mid;
       }
       r = lo;
-      const int32_t *row = L.rows + r * w;
-      const int32_t a = L.anc[r];
-      x0 = __ldg(adj + __ldg(off + a) + (j - L.pref[r]));
-      if (!WRITE) ++my_cand;
-      if (accept<!WRITE>(st, 0, row, w, 0, x0, L.acol[r], off, adj, my_probe)) {
-        if (st.n_new == 1) {
-          ns = 1;
-        } else {
-          int32_t av;
-          int64_t ad;
-          const int ac = pick_anchor(st, 1, row, w, x0, off, av, ad);
-          const int64_t e0 = __ldg(off + av);
-          for (int64_t e = e0; e < e0 + ad; ++e) {
-            const int32_t x1 = __ldg(adj + e);
-            if (!WRITE) ++my_cand;
-            if (accept<!WRITE>(st, 1, row, w, x0, x1, ac, off, adj, my_probe)) ++ns;
-          }
-        }
-      }
+      x0 = __ldg(adj + __ldg(off + L.anc[r]) + (j - L.pref[r]));
+      ++my_cand;
+      ok = accept(st, 0, L.rows + r * w, w, 0, x0, L.acol[r], off, adj, my_probe);
     }
-    if (!WRITE) {
-      my_surv += ns;
+    if (st.n_new == 1) {
+      emit(ok, r, x0, -1);
       continue;
     }
-    // ---- 4. (write) stage survivors, flush when the buffer would overflow
-    int pos, rtot;
-    ScanI(tmp.i).ExclusiveSum(ns, pos, rtot);
-    if (fill + rtot > kSurvBuf) {
-      __syncthreads();
-      flush_rows(L, w, W, fill, io.out, base);
-      __syncthreads();
-      base += fill;
-      fill = 0;
+    // second new vertex: candidate space over this round's accepted first vertices
+    long long d1 = 0;
+    if (ok) {
+      int32_t av;
+      int64_t ad;
+      L.aacol[tid] = pick_anchor(st, 1, L.rows + r * w, w, x0, off, av, ad);
+      L.aav[tid] = av;
+      L.ar[tid] = r;
+      L.ax0[tid] = x0;
+      d1 = ad;
     }
-    if (rtot > kSurvBuf) {
-      // hub rows: this round alone overflows the buffer -> write directly (uncoalesced, rare)
-      if (ns) {
-        const int32_t *row = L.rows + r * w;
-        int64_t o = base + pos;
-        auto put = [&](int32_t x1) {
-          int32_t *dst = io.out + o * W;
-          for (int c = 0; c < w; ++c) dst[c] = row[c];
-          dst[w] = x0;
-          if (st.n_new == 2) dst[w + 1] = x1;
-          ++o;
-        };
-        if (st.n_new == 1) {
-          put(-1);
-        } else {
-          int32_t av;
-          int64_t ad;
-          const int ac = pick_anchor(st, 1, row, w, x0, off, av, ad);
-          const int64_t e0 = __ldg(off + av);
-          uint64_t dummy = 0;
-          for (int64_t e = e0; e < e0 + ad; ++e) {
-            const int32_t x1 = __ldg(adj + e);
-            if (accept<false>(st, 1, row, w, x0, x1, ac, off, adj, dummy)) put(x1);
-          }
+    long long p1, C1;
+    ScanLL(tmp.ll).ExclusiveSum(d1, p1, C1);
+    L.apref[tid] = p1;
+    __syncthreads();
+    for (long long q0 = 0; q0 < C1; q0 += kStepThreads) {
+      const long long q = q0 + tid;
+      int ra = 0;
+      int32_t xa = -1, x1 = -1;
+      bool ok1 = false;
+      if (q < C1) {
+        int lo = 0, hi = kStepThreads;  // largest t with apref[t] <= q
+        while (hi - lo > 1) {
+          int mid = (lo + hi) >> 1;
+          if (L.apref[mid] <= q) lo = mid;
+          else hi = mid;
         }
+        ra = L.ar[lo];
+        xa = L.ax0[lo];
+        x1 = __ldg(adj + __ldg(off + L.aav[lo]) + (q - L.apref[lo]));
+        ++my_cand;
+        ok1 = accept(st, 1, L.rows + ra * w, w, xa, x1, L.aacol[lo], off, adj, my_probe);
       }
-      base += rtot;
-      __syncthreads();
-      continue;
+      emit(ok1, ra, xa, x1);
     }
-    if (ns) {
-      int p = fill + pos;
-      if (st.n_new == 1) {
-        L.sv_row[p] = r;
-        L.sv_x[2 * p] = x0;
-      } else {
-        const int32_t *row = L.rows + r * w;
-        int32_t av;
-        int64_t ad;
-        const int ac = pick_anchor(st, 1, row, w, x0, off, av, ad);
-        const int64_t e0 = __ldg(off + av);
-        uint64_t dummy = 0;
-        for (int64_t e = e0; e < e0 + ad; ++e) {
-          const int32_t x1 = __ldg(adj + e);
-          if (accept<false>(st, 1, row, w, x0, x1, ac, off, adj, dummy)) {
-            L.sv_row[p] = r;
-            L.sv_x[2 * p] = x0;
-            L.sv_x[2 * p + 1] = x1;
-            ++p;
-          }
-        }
-      }
-    }
-    fill += rtot;
-    __syncthreads();  // scan temp storage reuse + staged entries visible
+    __syncthreads();  // second-vertex arrays are rewritten next round
   }
 
-  if (WRITE) {
+  // ---- 4. finish
+  if (MODE == kModeWrite) {
     __syncthreads();
     flush_rows(L, w, W, fill, io.out, base);
     return;
   }
-  // ---- 4. (count) tile total + statistics
-  unsigned long long t = RedU(tmp.r).Sum((unsigned long long)my_surv);
-  __syncthreads();
-  unsigned long long tc = RedU(tmp.r).Sum((unsigned long long)my_cand);
-  __syncthreads();
-  unsigned long long tp = RedU(tmp.r).Sum((unsigned long long)my_probe);
-  if (tid == 0) {
-    if (io.block_cnt) io.block_cnt[tile] = t;
-    if (io.total) atomicAdd(io.total, t);
-    if (io.stats) {
+  if (io.stats) {
+    unsigned long long tc = RedU(tmp.r).Sum((unsigned long long)my_cand);
+    __syncthreads();
+    unsigned long long tp = RedU(tmp.r).Sum((unsigned long long)my_probe);
+    __syncthreads();
+    if (tid == 0) {
       atomicAdd(io.stats, tc);
       atomicAdd(io.stats + 1, tp);
     }
   }
+  if (MODE == kModeCount) {
+    unsigned long long t = RedU(tmp.r).Sum(my_surv);
+    if (tid == 0) {
+      if (io.block_cnt) io.block_cnt[tile] = t;
+      if (io.total) atomicAdd(io.total, t);
+    }
+    return;
+  }
+  // kModeSingle: decoupled look-back for the tile's exclusive prefix
+  if (tid == 0) {
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      st_volatile(io.status, kFlagPrefix | (unsigned long long)agg);
+    } else {
+      st_volatile(io.status + tile, kFlagAgg | (unsigned long long)agg);
+      int64_t p = tile - 1;
+      while (true) {
+        unsigned long long v = ld_volatile(io.status + p);
+        if (v == 0) continue;  // predecessor not published yet (dynamic ids: it is resident)
+        excl += v & kValueMask;
+        if (v & kFlagPrefix) break;
+        --p;
+      }
+      st_volatile(io.status + tile, kFlagPrefix | (excl + (unsigned long long)agg));
+    }
+    atomicAdd(io.ctrl + 2, (unsigned long long)agg);
+    const bool fits = !ovf && excl + (unsigned long long)agg <= io.cap;
+    if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
+    s_bc = fits ? excl : ~0ull;
+  }
+  __syncthreads();
+  if (s_bc != ~0ull) flush_rows(L, w, W, fill, io.out, (int64_t)s_bc);
 }
 
-}  // namespace
+// exclusive prefix over tiles from the look-back status words: excl[t] = inclusive[t-1]
+__global__ void k_status_to_excl(const unsigned long long *__restrict__ status, int64_t tiles,
+                                 uint64_t *__restrict__ excl) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= tiles;
+       t += (int64_t)gridDim.x * blockDim.x)
+    excl[t] = t == 0 ? 0 : (status[t - 1] & kValueMask);
+}
 
-size_t step_smem_bytes(int in_w, bool write_pass) { return smem_bytes(in_w, write_pass); }
-
-// Raise the dynamic shared-memory limit of a kernel once per (device, size) growth.
-static cudaError_t prep(const void *fn, int which, size_t smem) {
+// Raise the dynamic shared-memory limit of a kernel once per (device, kernel) growth.
+cudaError_t prep(const void *fn, int which, size_t smem) {
   static std::mutex mu;
-  static size_t configured[64][2] = {};
+  static size_t configured[64][3] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -371,23 +480,42 @@ static cudaError_t prep(const void *fn, int which, size_t smem) {
   return e;
 }
 
+template <int MODE>
+cudaError_t launch(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t num_tiles,
+                   cudaStream_t s) {
+  if (num_tiles <= 0) return cudaSuccess;
+  size_t smem = smem_bytes(st.in_w, MODE != kModeCount);
+  cudaError_t e = prep((const void *)k_step<MODE>, MODE, smem);
+  if (e != cudaSuccess) return e;
+  k_step<MODE><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+size_t step_smem_bytes(int in_w, bool write_pass) { return smem_bytes(in_w, write_pass); }
+
 cudaError_t launch_step_count(const DevStep &st, const StepIO &io, const dm_graph &g,
                               int64_t num_tiles, cudaStream_t s) {
-  if (num_tiles <= 0) return cudaSuccess;
-  size_t smem = smem_bytes(st.in_w, false);
-  cudaError_t e = prep((const void *)k_step<false>, 0, smem);
-  if (e != cudaSuccess) return e;
-  k_step<false><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
-  return cudaGetLastError();
+  return launch<kModeCount>(st, io, g, num_tiles, s);
 }
 
 cudaError_t launch_step_write(const DevStep &st, const StepIO &io, const dm_graph &g,
                               int64_t num_tiles, cudaStream_t s) {
-  if (num_tiles <= 0) return cudaSuccess;
-  size_t smem = smem_bytes(st.in_w, true);
-  cudaError_t e = prep((const void *)k_step<true>, 1, smem);
-  if (e != cudaSuccess) return e;
-  k_step<true><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
+  return launch<kModeWrite>(st, io, g, num_tiles, s);
+}
+
+cudaError_t launch_step_single(const DevStep &st, const StepIO &io, const dm_graph &g,
+                               int64_t num_tiles, cudaStream_t s) {
+  return launch<kModeSingle>(st, io, g, num_tiles, s);
+}
+
+cudaError_t launch_status_to_excl(const unsigned long long *status, int64_t tiles, uint64_t *excl,
+                                  cudaStream_t s) {
+  int64_t b = (tiles + 1 + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 2048) b = 2048;
+  k_status_to_excl<<<(unsigned)b, 256, 0, s>>>(status, tiles, excl);
   return cudaGetLastError();
 }
 

@@ -4,16 +4,20 @@
 //   R := seed (the first slice's table, reading Q3 of DESIGN.md: R <- {} then InnerJoin means
 //        "R becomes the first slice's table"; here the seed is the first join step applied to
 //        the implicit one-column table of all data vertices in [seed_begin, seed_end))
-//   for each step: count pass -> exclusive scan of tile counts -> write pass (two-pass emit)
-//   last step in count mode: count pass only (the last level is never materialized)
+//   for each step: one single-pass launch (join + filters + decoupled look-back prefix + write)
+//       into a buffer sized from the observed growth ratio; tiles that do not fit are re-run
+//       at their exact offsets (kModeWrite) -- count-then-write only where needed
+//   last step in count mode: count-only launch (the last level is never materialized)
 //
 // Frontier memory is bounded by chunking (depth-first across chunks, breadth-first inside a
-// chunk): when a level would exceed mem_budget bytes, its tiles are cut into groups whose
-// output fits (the count pass gives exact per-tile sizes) and each group is expanded to the
-// end before the next one is written.  Results do not depend on the chunking.
+// chunk): a level may use at most half of the device memory still free (or the caller's
+// mem_budget); a larger level is cut into groups of tiles whose output fits (exact sizes from
+// the look-back prefix) and each group is expanded to the end before the next one is
+// written.  Results do not depend on the chunking.
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <new>
 #include <vector>
@@ -118,12 +122,15 @@ struct Ctx {
   const Plan *plan = nullptr;
   cudaStream_t s = nullptr;
   bool table = false;
-  uint64_t mem_budget = 0;
+  uint64_t mem_budget = 0;  // caller's fixed per-chunk budget (0 = dynamic)
+  uint64_t mem_total = 0;   // dynamic: usable device bytes at the start of the match
+  uint64_t live = 0;        // bytes of frontier buffers currently held by the recursion
   uint64_t row_budget = 0;
   std::vector<DevStep> dsteps;
   unsigned long long *d_acc = nullptr;  // [0] count-mode total, [1+2i] C_i, [2+2i] Q_i
   int32_t *d_res = nullptr;             // table mode: rows in column (match) order
   uint64_t res_rows = 0, res_cap = 0;
+  std::vector<double> ratio;            // observed output/input rows per step (capacity estimate)
   dm_match_stats st;
   Prof prof;
 };
@@ -152,7 +159,8 @@ struct DevBuf {
   }
 };
 
-dm_status grow_result(Ctx &c, uint64_t need, int W) {
+// Ensure the result table can hold `need` rows; keeps the first `valid` rows.
+dm_status grow_result(Ctx &c, uint64_t need, uint64_t valid, int W) {
   if (need <= c.res_cap) return DM_OK;
   if (need > c.row_budget)
     return fail(DM_ERR_ROW_BUDGET, "result table exceeds row_budget (" + std::to_string(need) +
@@ -161,13 +169,34 @@ dm_status grow_result(Ctx &c, uint64_t need, int W) {
   cap = std::min<uint64_t>(cap, std::max<uint64_t>(need, c.row_budget));
   int32_t *p = nullptr;
   CK(cudaMallocAsync((void **)&p, sizeof(int32_t) * (size_t)cap * W, c.s), "result allocation");
-  if (c.res_rows)
-    CK(cudaMemcpyAsync(p, c.d_res, sizeof(int32_t) * (size_t)c.res_rows * W,
-                       cudaMemcpyDeviceToDevice, c.s),
+  if (valid)
+    CK(cudaMemcpyAsync(p, c.d_res, sizeof(int32_t) * (size_t)valid * W, cudaMemcpyDeviceToDevice, c.s),
        "result copy");
   if (c.d_res) cudaFreeAsync(c.d_res, c.s);
   c.d_res = p;
   c.res_cap = cap;
+  return DM_OK;
+}
+
+dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t seed_base);
+
+// kModeWrite over tiles [b0, b1) with exclusive tile prefix d_excl (global row numbering);
+// output row 0 of `out` corresponds to global row out_base.
+dm_status write_tiles(Ctx &c, int si, const StepIO &base_io, const uint64_t *d_excl, int64_t b0,
+                      int64_t b1, int32_t *out, uint64_t out_base) {
+  StepIO io = base_io;
+  io.block_off = d_excl;
+  io.block_begin = b0;
+  io.out = out;
+  io.out_base = out_base;
+  io.stats = nullptr;
+  io.block_cnt = nullptr;
+  io.total = nullptr;
+  Prof::Ev e;
+  c.prof.begin(si, 1, e);
+  CK(launch_step_write(c.dsteps[(size_t)si], io, *c.g, b1 - b0, c.s), "write kernel");
+  c.prof.end(e);
+  c.st.num_launches++;
   return DM_OK;
 }
 
@@ -198,89 +227,128 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     return DM_OK;
   }
 
-  DevBuf<uint64_t> cnt, scan;
-  CK(cnt.alloc((size_t)tiles + 1, c.s), "tile counts");
-  CK(scan.alloc((size_t)tiles + 1, c.s), "tile scan");
-  io.block_cnt = cnt.p;
-  {
-    Prof::Ev e;
-    c.prof.begin(si, 0, e);
-    CK(cudaMemsetAsync(cnt.p + tiles, 0, sizeof(uint64_t), c.s), "memset");
-    CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
-    c.prof.end(e);
-    c.st.num_launches++;
+  // ---- single pass (decoupled look-back) into an estimated-capacity buffer
+  const uint64_t row_bytes = (uint64_t)W * sizeof(int32_t);
+  const uint64_t avail =
+      c.mem_budget ? c.mem_budget : (c.mem_total > c.live ? (c.mem_total - c.live) / 2 : 0);
+  const uint64_t budget_rows = std::max<uint64_t>(1, avail / row_bytes);
+  struct Live {
+    Ctx &c;
+    uint64_t b = 0;
+    void add(uint64_t x) { b += x; c.live += x; }
+    ~Live() { c.live -= b; }
+  } live{c};
+  double ratio = c.ratio[(size_t)si];
+  if (ratio <= 0) {
+    const double avg = c.g->n ? (double)c.g->arcs / (double)c.g->n : 1.0;
+    ratio = std::pow(std::max(avg, 1.0), D.n_new);
   }
-  {
-    Prof::Ev e;
-    c.prof.begin(si, 2, e);
-    size_t tb = 0;
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.p, scan.p, tiles + 1, c.s), "scan");
-    DevBuf<unsigned char> tmp;
-    CK(tmp.alloc(tb, c.s), "scan temp");
-    CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.p, scan.p, tiles + 1, c.s), "scan");
-    c.prof.end(e);
-    c.st.num_launches++;
-  }
-  uint64_t total = 0;
-  CK(cudaMemcpyAsync(&total, scan.p + tiles, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s), "D2H");
-  CK(cudaStreamSynchronize(c.s), "sync");
-  c.st.rows_out[si] += total;
-  if (total == 0) return DM_OK;
-  io.block_cnt = nullptr;
-  io.stats = nullptr;
-  io.block_off = scan.p;
-
+  uint64_t cap = (uint64_t)((double)in_rows * ratio * 1.15) + 4096;
+  cap = std::min<uint64_t>(cap, budget_rows);
+  int32_t *out = nullptr;
+  DevBuf<int32_t> outb;
   if (last) {  // table mode: append to the result table
-    dm_status stt = grow_result(c, c.res_rows + total, W);
+    cap = std::min<uint64_t>(cap, c.row_budget - std::min(c.row_budget, c.res_rows));
+    if (cap == 0) cap = 1;
+    dm_status stt = grow_result(c, c.res_rows + cap, c.res_rows, W);
     if (stt != DM_OK) return stt;
-    io.out = c.d_res + (size_t)c.res_rows * W;
-    io.out_base = 0;
+    cap = c.res_cap - c.res_rows;
+    out = c.d_res + (size_t)c.res_rows * W;
+  } else {
+    CK(outb.alloc((size_t)cap * W, c.s), "frontier allocation");
+    live.add(cap * row_bytes);
+    out = outb.p;
+  }
+  DevBuf<unsigned long long> status, ctrl;
+  CK(status.alloc((size_t)tiles, c.s), "status");
+  CK(ctrl.alloc(3, c.s), "ctrl");
+  unsigned long long hctrl[3] = {0ull, (unsigned long long)tiles, 0ull};
+  CK(cudaMemsetAsync(status.p, 0, sizeof(unsigned long long) * (size_t)tiles, c.s), "memset");
+  CK(cudaMemcpyAsync(ctrl.p, hctrl, sizeof(hctrl), cudaMemcpyHostToDevice, c.s), "H2D ctrl");
+  io.status = status.p;
+  io.ctrl = ctrl.p;
+  io.cap = cap;
+  io.out = out;
+  {
     Prof::Ev e;
     c.prof.begin(si, 1, e);
-    CK(launch_step_write(D, io, *c.g, tiles, c.s), "write kernel");
+    CK(launch_step_single(D, io, *c.g, tiles, c.s), "single-pass kernel");
     c.prof.end(e);
     c.st.num_launches++;
+  }
+  CK(cudaMemcpyAsync(hctrl, ctrl.p, sizeof(hctrl), cudaMemcpyDeviceToHost, c.s), "D2H ctrl");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  const uint64_t total = hctrl[2];
+  const int64_t tstar = (int64_t)hctrl[1];
+  c.st.rows_out[si] += total;
+  c.ratio[(size_t)si] = (double)total / (double)in_rows;
+  if (total == 0) return DM_OK;
+
+  if (tstar >= tiles) {  // every tile written
+    if (last) {
+      c.res_rows += total;
+      return DM_OK;
+    }
+    return run_step(c, si + 1, out, (int64_t)total, 0);
+  }
+  c.st.reserved++;  // re-run count (tiles that did not fit)
+  // ---- some tiles did not fit: exact tile prefix from the look-back status words
+  DevBuf<uint64_t> excl;
+  CK(excl.alloc((size_t)tiles + 1, c.s), "excl");
+  CK(launch_status_to_excl(status.p, tiles, excl.p, c.s), "status->excl");
+  uint64_t written = 0;  // rows [0, written) are complete in `out`
+  CK(cudaMemcpyAsync(&written, excl.p + tstar, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s), "D2H");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  if (last) {
+    dm_status stt = grow_result(c, c.res_rows + total, c.res_rows + written, W);
+    if (stt != DM_OK) return stt;
+    stt = write_tiles(c, si, io, excl.p, tstar, tiles, c.d_res + (size_t)c.res_rows * W, 0);
+    if (stt != DM_OK) return stt;
     c.res_rows += total;
     return DM_OK;
   }
-
-  const uint64_t row_bytes = (uint64_t)W * sizeof(int32_t);
-  if (total * row_bytes <= c.mem_budget) {
-    DevBuf<int32_t> out;
-    CK(out.alloc((size_t)total * W, c.s), "frontier allocation");
-    io.out = out.p;
-    io.out_base = 0;
-    Prof::Ev e;
-    c.prof.begin(si, 1, e);
-    CK(launch_step_write(D, io, *c.g, tiles, c.s), "write kernel");
-    c.prof.end(e);
-    c.st.num_launches++;
-    return run_step(c, si + 1, out.p, (int64_t)total, 0);
+  if (total <= budget_rows) {
+    if (total > cap) {
+      DevBuf<int32_t> bigger;
+      CK(bigger.alloc((size_t)total * W, c.s), "frontier allocation");
+      live.add(total * row_bytes);
+      if (written)
+        CK(cudaMemcpyAsync(bigger.p, out, sizeof(int32_t) * (size_t)written * W,
+                           cudaMemcpyDeviceToDevice, c.s),
+           "frontier copy");
+      std::swap(outb.p, bigger.p);
+      out = outb.p;
+    }
+    dm_status stt = write_tiles(c, si, io, excl.p, tstar, tiles, out, 0);
+    if (stt != DM_OK) return stt;
+    return run_step(c, si + 1, out, (int64_t)total, 0);
   }
-  // chunked: groups of tiles whose output fits the budget
+  // ---- chunked: the written prefix first, then groups of tiles whose output fits
   std::vector<uint64_t> h((size_t)tiles + 1);
-  CK(cudaMemcpyAsync(h.data(), scan.p, sizeof(uint64_t) * ((size_t)tiles + 1),
+  CK(cudaMemcpyAsync(h.data(), excl.p, sizeof(uint64_t) * ((size_t)tiles + 1),
                      cudaMemcpyDeviceToHost, c.s),
-     "D2H scan");
+     "D2H excl");
   CK(cudaStreamSynchronize(c.s), "sync");
-  const uint64_t budget_rows = std::max<uint64_t>(1, c.mem_budget / row_bytes);
-  int64_t b0 = 0;
+  if (written) {
+    dm_status stt = run_step(c, si + 1, out, (int64_t)written, 0);
+    if (stt != DM_OK) return stt;
+  }
+  if (outb.p) {
+    cudaFreeAsync(outb.p, c.s);
+    outb.p = nullptr;
+  }
+  int64_t b0 = tstar;
   while (b0 < tiles) {
     int64_t b1 = b0 + 1;
     while (b1 < tiles && h[(size_t)b1 + 1] - h[(size_t)b0] <= budget_rows) ++b1;
     const uint64_t rows = h[(size_t)b1] - h[(size_t)b0];
     if (rows > 0) {
-      DevBuf<int32_t> out;
-      CK(out.alloc((size_t)rows * W, c.s), "frontier chunk allocation");
-      io.out = out.p;
-      io.out_base = h[(size_t)b0];
-      io.block_begin = b0;
-      Prof::Ev e;
-      c.prof.begin(si, 1, e);
-      CK(launch_step_write(D, io, *c.g, b1 - b0, c.s), "write kernel");
-      c.prof.end(e);
-      c.st.num_launches++;
-      dm_status stt = run_step(c, si + 1, out.p, (int64_t)rows, 0);
+      DevBuf<int32_t> chunk;
+      CK(chunk.alloc((size_t)rows * W, c.s), "frontier chunk allocation");
+      live.add(rows * row_bytes);
+      dm_status stt = write_tiles(c, si, io, excl.p, b0, b1, chunk.p, h[(size_t)b0]);
+      if (stt != DM_OK) return stt;
+      stt = run_step(c, si + 1, chunk.p, (int64_t)rows, 0);
       if (stt != DM_OK) return stt;
     }
     b0 = b1;
@@ -371,17 +439,24 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   std::memset(&c.st, 0, sizeof(c.st));
   c.st.num_steps = (int32_t)plan.steps.size();
   for (auto &s : plan.steps) c.dsteps.push_back(make_dev_step(s));
+  c.ratio.assign(plan.steps.size(), 0.0);
   for (size_t i = 0; i < plan.steps.size(); ++i) {
     c.st.width_in[i] = plan.steps[i].in_w;
     c.st.width_out[i] = plan.steps[i].in_w + plan.steps[i].n_new;
   }
-  if (opt.mem_budget) {
-    c.mem_budget = opt.mem_budget;
-  } else {
+  c.mem_budget = opt.mem_budget;
+  if (!c.mem_budget) {
     size_t fr = 0, tot = 0;
     CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
-    uint64_t per = (uint64_t)(fr * 0.7) / (uint64_t)(plan.steps.size() + 2);
-    c.mem_budget = std::max<uint64_t>(per, 64ull << 20);
+    // memory already cached by the stream-ordered pool is reusable too
+    cudaMemPool_t pool;
+    uint64_t reserved = 0, used = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+    }
+    c.mem_total = std::max<uint64_t>((uint64_t)((double)(fr + (reserved - std::min(reserved, used))) * 0.85),
+                                     256ull << 20);
   }
   c.prof.on = (opt.flags & DM_MATCH_PROFILE) != 0;
   c.prof.s = c.s;
