@@ -44,9 +44,16 @@ struct DeviceGuard {
 constexpr int kStepThreads = 256;   // threads per CTA
 constexpr int kTileRows = 256;      // frontier rows per CTA tile
 constexpr int kSurvBuf = 1024;      // survivors staged in shared memory per CTA
+constexpr int kRowSlots = 8;        // row-serial kernel: survivor slots per frontier row
+constexpr int kRowSerialDeg1 = 16;  // row-serial kernel for 1-vertex steps if max degree <= 16
+constexpr int kRowSerialDeg2 = 6;   //   ... and for 2-vertex steps if max degree <= 6
 constexpr int kModeCount = 0;       // join-step kernel launch modes (see extend.cu)
 constexpr int kModeWrite = 1;
 constexpr int kModeSingle = 2;
+
+// Frontier rows are stored with a 16-byte aligned stride: row_stride(w) int32 words, the
+// padding words hold -1 (never a vertex id).
+__host__ __device__ inline int row_stride(int w) { return (w + 3) & ~3; }
 
 // Device copy of one executed step (passed by value as a kernel parameter).
 struct DevStep {
@@ -59,11 +66,11 @@ struct DevStep {
 };
 
 struct StepIO {
-  const int32_t *in;          // [in_rows][in_w] row-major, or nullptr for the implicit seed
+  const int32_t *in;          // [in_rows][row_stride(in_w)], or nullptr for the implicit seed
   int64_t in_rows;            // rows of this launch's input (chunk)
   int64_t seed_base;          // implicit seed: row r is vertex seed_base + r
   int64_t block_begin;        // first tile index of this launch (chunked write passes)
-  int32_t *out;               // write pass: [*][in_w + n_new]
+  int32_t *out;               // write pass: [*][row_stride(in_w + n_new)]
   const uint64_t *block_off;  // write pass: exclusive prefix of survivors per tile (global)
   uint64_t out_base;          // write pass: block_off value that maps to out row 0
   uint64_t *block_cnt;        // count pass: survivors per tile (nullptr -> only total)

@@ -46,12 +46,19 @@ struct Step {
   StepVertex nv[2];
 };
 
+// Data-graph statistics for the join-order cost model (defaults: a sparse lattice).
+struct PlanStats {
+  double n = 10000.0;
+  double avg_degree = 3.0;
+};
+
 struct Plan {
   int k = 0;
   int mode = DM_MONO;
   int motifs = DM_MOTIF_M2;
   std::vector<std::pair<int, int>> edges;  // deduplicated pattern edges (a < b)
   std::vector<Slice> slices;
+  std::vector<int> order;      // slice execution order (left-deep)
   std::vector<Step> steps;
   std::vector<int> col_pvert;  // column -> pattern vertex (match order)
   std::vector<int> pvert_col;  // pattern vertex -> column
@@ -61,7 +68,7 @@ struct Plan {
 
 // Validates the pattern and builds the plan.  Returns DM_OK or an error (message set).
 dm_status build_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs, int32_t mode,
-                     Plan &out);
+                     Plan &out, const PlanStats &stats = PlanStats());
 
 }  // namespace dm
 

@@ -12,9 +12,12 @@
 // probed by binary search in the shorter of the two adjacency lists.
 //
 // CTA = one tile of kTileRows consecutive frontier rows (one contiguous block of memory):
-//   1. tile -> shared memory with one TMA bulk copy (cp.async.bulk + mbarrier);
+//   1. tile -> shared memory with one TMA bulk copy (cp.async.bulk + mbarrier); frontier rows
+//      are stored with a 16-byte stride (row_stride(w) words, padding = -1), so every row is
+//      int4-aligned: LDS.128 all-distinct tests and STG.128 row writes;
 //   2. per row: join key (anchor) of the first new vertex, candidate count = its degree; CTA
-//      exclusive scan -> the tile's candidate space (a hub row is spread over the CTA);
+//      exclusive scan -> the tile's candidate space (a hub row is spread over the CTA); each
+//      round maps candidates to rows by scattering segment starts + a max-scan;
 //   3. rounds of kStepThreads candidates: injectivity + closing-edge (+ induced non-edge)
 //      probes; for 2-vertex steps (wedge / triangle slices) the accepted first vertices of the
 //      round and their second-vertex candidate counts are scanned again, so every second-level
@@ -67,17 +70,27 @@ __device__ __forceinline__ bool has_edge(const int64_t *__restrict__ off,
   return lo < end && __ldg(adj + lo) == key;
 }
 
-// x in row?  branch-free, unrolled by 4 (rows sit at stride w in shared memory; for odd w a
-// warp's rows fall in distinct banks).
-__device__ __forceinline__ bool in_row(const int32_t *row, int w, int32_t x) {
+// x in row?  The row is 16-byte aligned and padded with -1 to ws words (a multiple of 4),
+// so the all-distinct test is ws/4 LDS.128 + compares, branch-free.  Rows sit at stride ws in
+// shared memory; when ws/4 is even, consecutive rows would start in the same bank group, so
+// each row starts its scan at chunk `rot` (= row index mod ws/4) -> conflict-free LDS.128.
+__device__ __forceinline__ bool in_row(const int32_t *row, int ws, int rot, int32_t x) {
+  const int4 *r4 = reinterpret_cast<const int4 *>(row);
+  const int nq = ws >> 2;
   bool hit = false;
-  int c = 0;
-  for (; c + 4 <= w; c += 4) {
-    const int32_t a = row[c], b = row[c + 1], d = row[c + 2], e = row[c + 3];
-    hit |= (a == x) | (b == x) | (d == x) | (e == x);
+  int idx = rot;
+#pragma unroll 4
+  for (int q = 0; q < nq; ++q) {
+    const int4 v = r4[idx];
+    hit |= (v.x == x) | (v.y == x) | (v.z == x) | (v.w == x);
+    idx = idx + 1 == nq ? 0 : idx + 1;
   }
-  for (; c < w; ++c) hit |= row[c] == x;
   return hit;
+}
+
+__device__ __forceinline__ int row_rot(int r, int ws) {
+  const int nq = ws >> 2;
+  return (nq & 1) ? 0 : r % nq;
 }
 
 // ---- TMA 1-D bulk copy global -> shared, completion tracked by an mbarrier (sm_90+ / sm_100a)
@@ -118,11 +131,11 @@ __device__ __forceinline__ int32_t colval(const int32_t *row, int w, int c, int3
 
 // Filters for new vertex j with candidate value x (anchor column `acol` is satisfied by
 // construction): all-distinct, closing-edge probes, induced non-edge probes.
-__device__ __forceinline__ bool accept(const DevStep &st, int j, const int32_t *row, int w,
-                                       int32_t x0, int32_t x, int acol,
+__device__ __forceinline__ bool accept(const DevStep &st, int j, const int32_t *row, int w, int ws,
+                                       int rot, int32_t x0, int32_t x, int acol,
                                        const int64_t *__restrict__ off,
                                        const int32_t *__restrict__ adj, uint32_t &probes) {
-  if (in_row(row, w, x)) return false;
+  if (in_row(row, ws, rot, x)) return false;
   if (j == 1 && x == x0) return false;
   for (int t = 0; t < st.n_nbr[j]; ++t) {
     int c = st.nbr[j][t];
@@ -160,25 +173,29 @@ __device__ __forceinline__ int pick_anchor(const DevStep &st, int j, const int32
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 struct SmemLayout {
-  int32_t *rows;     // [kTileRows][w] (the tile, contiguous as in global memory)
-  long long *pref;   // [kTileRows]    first-vertex candidate prefix
-  int32_t *anc;      // [kTileRows]    first-vertex anchor vertex
+  int32_t *rows;     // [kTileRows][ws] the tile exactly as stored in global memory
+  long long *pref;   // [kTileRows+1]  first-vertex candidate prefix (pref[nrows] = C0)
+  long long *abeg;   // [kTileRows]    CSR start of the first-vertex anchor's list
   int32_t *acol;     // [kTileRows]    first-vertex anchor column
-  long long *apref;  // [kStepThreads] second-vertex candidate prefix (per round)
+  int32_t *owner;    // [kStepThreads] candidate -> row / entry map of the current round
+  long long *apref;  // [kStepThreads+1] second-vertex candidate prefix (per round)
+  long long *aabeg;  // [kStepThreads] CSR start of the second-vertex anchor's list
   int32_t *ar;       // [kStepThreads] row of the accepted first vertex
   int32_t *ax0;      // [kStepThreads] accepted first vertex
-  int32_t *aav;      // [kStepThreads] second-vertex anchor vertex
   int32_t *aacol;    // [kStepThreads] second-vertex anchor column
   int32_t *sv_row;   // [kSurvBuf]
   int32_t *sv_x;     // [kSurvBuf][2]
 };
 
 __host__ __device__ inline size_t smem_bytes(int in_w, bool stage) {
-  size_t b = align16(sizeof(int32_t) * (size_t)kTileRows * in_w);
+  size_t b = align16(sizeof(int32_t) * (size_t)kTileRows * row_stride(in_w));
+  b += align16(sizeof(long long) * (kTileRows + 1));
   b += align16(sizeof(long long) * kTileRows);
-  b += 2 * align16(sizeof(int32_t) * kTileRows);
+  b += align16(sizeof(int32_t) * kTileRows);
+  b += align16(sizeof(int32_t) * kStepThreads);
+  b += align16(sizeof(long long) * (kStepThreads + 1));
   b += align16(sizeof(long long) * kStepThreads);
-  b += 4 * align16(sizeof(int32_t) * kStepThreads);
+  b += 3 * align16(sizeof(int32_t) * kStepThreads);
   if (stage) b += align16(sizeof(int32_t) * kSurvBuf) + align16(sizeof(int32_t) * 2 * kSurvBuf);
   return b;
 }
@@ -191,14 +208,15 @@ __device__ inline SmemLayout carve(unsigned char *base, int in_w, bool stage) {
     o += align16(bytes);
     return p;
   };
-  L.rows = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * (size_t)kTileRows * in_w));
-  L.pref = reinterpret_cast<long long *>(take(sizeof(long long) * kTileRows));
-  L.anc = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kTileRows));
+  L.rows = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * (size_t)kTileRows * row_stride(in_w)));
+  L.pref = reinterpret_cast<long long *>(take(sizeof(long long) * (kTileRows + 1)));
+  L.abeg = reinterpret_cast<long long *>(take(sizeof(long long) * kTileRows));
   L.acol = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kTileRows));
-  L.apref = reinterpret_cast<long long *>(take(sizeof(long long) * kStepThreads));
+  L.owner = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
+  L.apref = reinterpret_cast<long long *>(take(sizeof(long long) * (kStepThreads + 1)));
+  L.aabeg = reinterpret_cast<long long *>(take(sizeof(long long) * kStepThreads));
   L.ar = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
   L.ax0 = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
-  L.aav = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
   L.aacol = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kStepThreads));
   if (stage) {
     L.sv_row = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kSurvBuf));
@@ -209,27 +227,46 @@ __device__ inline SmemLayout carve(unsigned char *base, int in_w, bool stage) {
   return L;
 }
 
-// Write `fill` staged survivors as rows [base, base+fill) of out (width W): each warp writes
-// whole rows, lanes map to columns, consecutive rows are contiguous -> coalesced stores.
-__device__ __forceinline__ void flush_rows(const SmemLayout &L, int w, int W, int fill,
-                                           int32_t *__restrict__ out, int64_t base) {
+// Write `fill` staged survivors as rows [base, base+fill) of out (row stride Wp = stride(W)).
+// A row is Wp/4 int4 chunks; lpr lanes (power of two >= Wp/4) cover one row, so one warp
+// store instruction writes 32/lpr consecutive rows = a contiguous, 16-byte aligned span.
+// The new vertices are patched into the chunk that holds columns w, w+1.
+__device__ __forceinline__ void flush_rows(const int32_t *rows, const int32_t *sv_row,
+                                           const int32_t *sv_x, const int32_t *map, int w,
+                                           int n_new, int fill, int32_t *__restrict__ out,
+                                           int64_t base) {
+  const int ws = row_stride(w), Wp = row_stride(w + n_new);
+  const int nq = Wp >> 2, nqs = ws >> 2;
+  int lpr = 1;
+  while (lpr < nq) lpr <<= 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kStepThreads / 32;
-  if (W <= 32) {
-    const int rpi = 32 / W;
-    const int lr = lane / W, lc = lane - lr * W;
-    if (lr < rpi) {
-      for (int s = warp * rpi + lr; s < fill; s += nwarps * rpi) {
-        int32_t v = lc < w ? L.rows[L.sv_row[s] * w + lc] : L.sv_x[2 * s + (lc - w)];
-        out[(base + s) * W + lc] = v;
-      }
+  const int q = lane & (lpr - 1);
+  const int rpi = 32 / lpr;
+  const int sub = lane / lpr;
+  if (q >= nq) return;
+  const int c0 = q << 2;
+  const int k0 = w - c0, k1 = w + 1 - c0;  // component index of x0 / x1 in this chunk
+  const bool has0 = k0 >= 0 && k0 < 4, has1 = n_new == 2 && k1 >= 0 && k1 < 4;
+  int4 *out4 = reinterpret_cast<int4 *>(out);
+  for (int o = warp * rpi + sub; o < fill; o += nwarps * rpi) {
+    const int s = map ? map[o] : o;
+    int4 v = q < nqs ? reinterpret_cast<const int4 *>(rows + sv_row[s] * ws)[q]
+                     : make_int4(-1, -1, -1, -1);
+    if (has0) {
+      const int32_t x0 = sv_x[2 * s];
+      v.x = k0 == 0 ? x0 : v.x;
+      v.y = k0 == 1 ? x0 : v.y;
+      v.z = k0 == 2 ? x0 : v.z;
+      v.w = k0 == 3 ? x0 : v.w;
     }
-  } else {
-    for (int s = warp; s < fill; s += nwarps) {
-      for (int c = lane; c < W; c += 32) {
-        int32_t v = c < w ? L.rows[L.sv_row[s] * w + c] : L.sv_x[2 * s + (c - w)];
-        out[(base + s) * W + c] = v;
-      }
+    if (has1) {
+      const int32_t x1 = sv_x[2 * s + 1];
+      v.x = k1 == 0 ? x1 : v.x;
+      v.y = k1 == 1 ? x1 : v.y;
+      v.z = k1 == 2 ? x1 : v.z;
+      v.w = k1 == 3 ? x1 : v.w;
     }
+    out4[(base + o) * nq + q] = v;
   }
 }
 
@@ -238,6 +275,37 @@ __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long lo
 }
 __device__ __forceinline__ void st_volatile(unsigned long long *p, unsigned long long v) {
   *reinterpret_cast<volatile unsigned long long *>(p) = v;
+}
+
+// Decoupled look-back by warp 0: publish the tile aggregate, then scan 32 predecessors at a
+// time (ballot for the nearest inclusive prefix); returns the exclusive prefix to all lanes.
+__device__ unsigned long long lookback(unsigned long long *status, int64_t tile,
+                                       unsigned long long agg) {
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) st_volatile(status, kFlagPrefix | agg);
+    return 0;
+  }
+  if (lane == 0) st_volatile(status + tile, kFlagAgg | agg);
+  unsigned long long excl = 0;
+  int64_t hi = tile - 1;
+  while (true) {
+    const int64_t p = hi - lane;
+    const unsigned long long v = p >= 0 ? ld_volatile(status + p) : kFlagPrefix;
+    const unsigned pm = __ballot_sync(0xffffffffu, (v & kFlagPrefix) != 0);
+    const unsigned zm = __ballot_sync(0xffffffffu, v == 0);
+    const int fp = pm ? __ffs(pm) - 1 : 31;  // lanes 0..fp are needed
+    const unsigned need = fp >= 31 ? 0xffffffffu : ((1u << (fp + 1)) - 1u);
+    if (zm & need) continue;  // a needed predecessor has not published yet: re-read
+    unsigned long long val = lane <= fp ? (v & kValueMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+    excl += val;
+    if (pm) break;
+    hi -= 32;
+  }
+  if (lane == 0) st_volatile(status + tile, kFlagPrefix | (excl + agg));
+  return excl;
 }
 
 template <int MODE>
@@ -258,7 +326,7 @@ __global__ void __launch_bounds__(kStepThreads)
   constexpr bool kStage = MODE != kModeCount;
 
   const int w = st.in_w;
-  const int W = w + st.n_new;
+  const int ws = row_stride(w);
   const int tid = threadIdx.x;
   int64_t tile;
   if (MODE == kModeSingle) {
@@ -273,42 +341,35 @@ __global__ void __launch_bounds__(kStepThreads)
   const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
   SmemLayout L = carve(smem_raw, w, kStage);
 
-  // ---- 1. tile -> shared memory: one TMA bulk copy of the contiguous tile (16-byte multiple;
-  //         the <= 3-word tail of the last tile with plain loads), mbarrier completion
+  // ---- 1. tile -> shared memory: one TMA bulk copy (rows are 16-byte strided)
   if (io.in) {
-    const int32_t *src = io.in + r0 * w;
-    const int nw = nrows * w;
-    const unsigned bulk = (unsigned)(nw & ~3) * 4u;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(src) & 15) == 0);
-    if (aligned && bulk > 0) {
-      if (tid == 0) mbar_init(&s_bar, 1);
-      __syncthreads();
-      if (tid == 0) {
-        mbar_expect_tx(&s_bar, bulk);
-        tma_bulk_g2s(L.rows, src, bulk, &s_bar);
-      }
-      for (int i = (nw & ~3) + tid; i < nw; i += kStepThreads) L.rows[i] = __ldcs(src + i);
-      mbar_wait(&s_bar, 0);
-    } else {
-      for (int i = tid; i < nw; i += kStepThreads) L.rows[i] = __ldcs(src + i);
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      const unsigned bytes = (unsigned)(nrows * ws) * 4u;
+      mbar_expect_tx(&s_bar, bytes);
+      tma_bulk_g2s(L.rows, io.in + r0 * ws, bytes, &s_bar);
     }
-  } else {
-    for (int r = tid; r < nrows; r += kStepThreads) L.rows[r] = (int32_t)(io.seed_base + r0 + r);
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(&s_bar, 0);
+  } else {  // implicit seed table: row r = vertex seed_base + r0 + r
+    for (int r = tid; r < nrows; r += kStepThreads)
+      reinterpret_cast<int4 *>(L.rows)[r] = make_int4((int32_t)(io.seed_base + r0 + r), -1, -1, -1);
+    __syncthreads();
   }
-  __syncthreads();
 
   // ---- 2. per-row join key for the first new vertex; tile candidate space
   long long cnt = 0;
   if (tid < nrows) {
     int32_t av;
     int64_t ad;
-    L.acol[tid] = pick_anchor(st, 0, L.rows + tid * w, w, 0, off, av, ad);
-    L.anc[tid] = av;
+    L.acol[tid] = pick_anchor(st, 0, L.rows + tid * ws, w, 0, off, av, ad);
+    L.abeg[tid] = __ldg(off + av);
     cnt = ad;
   }
   long long pref, C0;
   ScanLL(tmp.ll).ExclusiveSum(cnt, pref, C0);
   L.pref[tid] = pref;
+  if (tid == 0) L.pref[nrows] = C0;
   __syncthreads();
 
   uint32_t my_cand = 0, my_probe = 0;
@@ -329,7 +390,7 @@ __global__ void __launch_bounds__(kStepThreads)
     ScanI(tmp.i).ExclusiveSum(s ? 1 : 0, pos, tot);
     if (MODE == kModeWrite && fill + tot > kSurvBuf) {
       __syncthreads();
-      flush_rows(L, w, W, fill, io.out, base);
+      flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, w, st.n_new, fill, io.out, base);
       __syncthreads();
       base += fill;
       fill = 0;
@@ -348,23 +409,32 @@ __global__ void __launch_bounds__(kStepThreads)
     __syncthreads();  // scan storage reuse
   };
 
+  // owner[t] = index i of the segment [pref[i], pref[i+1]) that holds candidate j0 + t:
+  // segment starts are scattered, then an inclusive max-scan fills the gaps.
+  auto map_round = [&](const long long *pf, int nseg, long long j0) {
+    L.owner[tid] = -1;
+    __syncthreads();
+    if (tid < nseg) {
+      const long long b = pf[tid], e = pf[tid + 1];
+      if (e > b && e > j0 && b < j0 + kStepThreads) L.owner[(b > j0 ? b : j0) - j0] = tid;
+    }
+    __syncthreads();
+    int o = L.owner[tid];
+    ScanI(tmp.i).InclusiveScan(o, o, cub::Max());
+    __syncthreads();
+    return o;
+  };
+
   // ---- 3. candidate rounds
   for (long long j0 = 0; j0 < C0; j0 += kStepThreads) {
     const long long j = j0 + tid;
-    int r = 0;
+    const int r = map_round(L.pref, nrows, j0);
     int32_t x0 = -1;
     bool ok = false;
     if (j < C0) {
-      int lo = 0, hi = nrows;  // largest r with pref[r] <= j
-      while (hi - lo > 1) {
-        int mid = (lo + hi) >> 1;
-        if (L.pref[mid] <= j) lo = mid;
-        else hi = mid;
-      }
-      r = lo;
-      x0 = __ldg(adj + __ldg(off + L.anc[r]) + (j - L.pref[r]));
+      x0 = __ldg(adj + L.abeg[r] + (j - L.pref[r]));
       ++my_cand;
-      ok = accept(st, 0, L.rows + r * w, w, 0, x0, L.acol[r], off, adj, my_probe);
+      ok = accept(st, 0, L.rows + r * ws, w, ws, row_rot(r, ws), 0, x0, L.acol[r], off, adj, my_probe);
     }
     if (st.n_new == 1) {
       emit(ok, r, x0, -1);
@@ -375,8 +445,8 @@ __global__ void __launch_bounds__(kStepThreads)
     if (ok) {
       int32_t av;
       int64_t ad;
-      L.aacol[tid] = pick_anchor(st, 1, L.rows + r * w, w, x0, off, av, ad);
-      L.aav[tid] = av;
+      L.aacol[tid] = pick_anchor(st, 1, L.rows + r * ws, w, x0, off, av, ad);
+      L.aabeg[tid] = __ldg(off + av);
       L.ar[tid] = r;
       L.ax0[tid] = x0;
       d1 = ad;
@@ -384,24 +454,20 @@ __global__ void __launch_bounds__(kStepThreads)
     long long p1, C1;
     ScanLL(tmp.ll).ExclusiveSum(d1, p1, C1);
     L.apref[tid] = p1;
+    if (tid == 0) L.apref[kStepThreads] = C1;
     __syncthreads();
     for (long long q0 = 0; q0 < C1; q0 += kStepThreads) {
       const long long q = q0 + tid;
+      const int t = map_round(L.apref, kStepThreads, q0);
       int ra = 0;
       int32_t xa = -1, x1 = -1;
       bool ok1 = false;
       if (q < C1) {
-        int lo = 0, hi = kStepThreads;  // largest t with apref[t] <= q
-        while (hi - lo > 1) {
-          int mid = (lo + hi) >> 1;
-          if (L.apref[mid] <= q) lo = mid;
-          else hi = mid;
-        }
-        ra = L.ar[lo];
-        xa = L.ax0[lo];
-        x1 = __ldg(adj + __ldg(off + L.aav[lo]) + (q - L.apref[lo]));
+        ra = L.ar[t];
+        xa = L.ax0[t];
+        x1 = __ldg(adj + L.aabeg[t] + (q - L.apref[t]));
         ++my_cand;
-        ok1 = accept(st, 1, L.rows + ra * w, w, xa, x1, L.aacol[lo], off, adj, my_probe);
+        ok1 = accept(st, 1, L.rows + ra * ws, w, ws, row_rot(ra, ws), xa, x1, L.aacol[t], off, adj, my_probe);
       }
       emit(ok1, ra, xa, x1);
     }
@@ -411,7 +477,7 @@ __global__ void __launch_bounds__(kStepThreads)
   // ---- 4. finish
   if (MODE == kModeWrite) {
     __syncthreads();
-    flush_rows(L, w, W, fill, io.out, base);
+    flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, w, st.n_new, fill, io.out, base);
     return;
   }
   if (io.stats) {
@@ -432,30 +498,166 @@ __global__ void __launch_bounds__(kStepThreads)
     }
     return;
   }
-  // kModeSingle: decoupled look-back for the tile's exclusive prefix
-  if (tid == 0) {
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      st_volatile(io.status, kFlagPrefix | (unsigned long long)agg);
-    } else {
-      st_volatile(io.status + tile, kFlagAgg | (unsigned long long)agg);
-      int64_t p = tile - 1;
-      while (true) {
-        unsigned long long v = ld_volatile(io.status + p);
-        if (v == 0) continue;  // predecessor not published yet (dynamic ids: it is resident)
-        excl += v & kValueMask;
-        if (v & kFlagPrefix) break;
-        --p;
-      }
-      st_volatile(io.status + tile, kFlagPrefix | (excl + (unsigned long long)agg));
+  // kModeSingle: decoupled look-back for the tile's exclusive prefix, then write
+  if (tid < 32) {
+    const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
+    if (tid == 0) {
+      atomicAdd(io.ctrl + 2, (unsigned long long)agg);
+      const bool fits = !ovf && excl + (unsigned long long)agg <= io.cap;
+      if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
+      s_bc = fits ? excl : ~0ull;
     }
-    atomicAdd(io.ctrl + 2, (unsigned long long)agg);
-    const bool fits = !ovf && excl + (unsigned long long)agg <= io.cap;
-    if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
-    s_bc = fits ? excl : ~0ull;
   }
   __syncthreads();
-  if (s_bc != ~0ull) flush_rows(L, w, W, fill, io.out, (int64_t)s_bc);
+  if (s_bc != ~0ull) flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, w, st.n_new, fill, io.out, (int64_t)s_bc);
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Row-serial variant for low-degree data graphs (lattices: max degree <= kRowSerialDeg):
+// thread = frontier row; the thread walks its join candidates (CSR range of the anchor key,
+// then of the second new vertex's key) serially, so a tile needs one CTA scan instead of
+// per-round scans and barriers.  Survivors go to per-thread slots (kRowSlots each); a thread
+// that overflows its slots marks the tile unwritten and the host re-runs it with the general
+// kernel (kModeWrite).  Output order is identical to k_step (row, then candidate order).
+template <int MODE>
+__global__ void __launch_bounds__(kStepThreads)
+    k_rows(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+           const int32_t *__restrict__ adj) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  typedef cub::BlockScan<int, kStepThreads> ScanI;
+  typedef cub::BlockReduce<unsigned long long, kStepThreads> RedU;
+  __shared__ union {
+    typename ScanI::TempStorage i;
+    typename RedU::TempStorage r;
+  } tmp;
+  __shared__ unsigned long long s_bc;
+  __shared__ __align__(8) uint64_t s_bar;
+  constexpr bool kStage = MODE != kModeCount;
+
+  const int w = st.in_w;
+  const int ws = row_stride(w);
+  const int tid = threadIdx.x;
+  int64_t tile;
+  if (MODE == kModeSingle) {
+    if (tid == 0) s_bc = atomicAdd(io.ctrl + 0, 1ull);
+    __syncthreads();
+    tile = (int64_t)s_bc;
+  } else {
+    tile = io.block_begin + blockIdx.x;
+  }
+  const int64_t r0 = tile * kTileRows;
+  if (r0 >= io.in_rows) return;
+  const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
+  int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
+  int32_t *sv_row = rows + kTileRows * ws;              // [kTileRows * kRowSlots]
+  int32_t *sv_x = sv_row + kTileRows * kRowSlots;       // [kTileRows * kRowSlots][2]
+  int32_t *map = sv_x + 2 * kTileRows * kRowSlots;      // [kTileRows * kRowSlots]
+
+  if (io.in) {
+    if (tid == 0) {
+      mbar_init(&s_bar, 1);
+      const unsigned bytes = (unsigned)(nrows * ws) * 4u;
+      mbar_expect_tx(&s_bar, bytes);
+      tma_bulk_g2s(rows, io.in + r0 * ws, bytes, &s_bar);
+    }
+    __syncthreads();
+    mbar_wait(&s_bar, 0);
+  } else {
+    for (int r = tid; r < nrows; r += kStepThreads)
+      reinterpret_cast<int4 *>(rows)[r] = make_int4((int32_t)(io.seed_base + r0 + r), -1, -1, -1);
+    __syncthreads();
+  }
+
+  int ns = 0;
+  bool ovf = false;
+  uint32_t my_cand = 0, my_probe = 0;
+  if (tid < nrows) {
+    const int32_t *row = rows + tid * ws;
+    const int rot = row_rot(tid, ws);
+    int32_t av;
+    int64_t ad;
+    const int ac = pick_anchor(st, 0, row, w, 0, off, av, ad);
+    const int64_t e0 = __ldg(off + av);
+    for (int64_t e = e0; e < e0 + ad; ++e) {
+      const int32_t x0 = __ldg(adj + e);
+      ++my_cand;
+      if (!accept(st, 0, row, w, ws, rot, 0, x0, ac, off, adj, my_probe)) continue;
+      if (st.n_new == 1) {
+        if (kStage) {
+          if (ns < kRowSlots) {
+            const int sl = tid * kRowSlots + ns;
+            sv_row[sl] = tid;
+            sv_x[2 * sl] = x0;
+          } else {
+            ovf = true;
+          }
+        }
+        ++ns;
+        continue;
+      }
+      int32_t bv;
+      int64_t bd;
+      const int bc = pick_anchor(st, 1, row, w, x0, off, bv, bd);
+      const int64_t f0 = __ldg(off + bv);
+      for (int64_t f = f0; f < f0 + bd; ++f) {
+        const int32_t x1 = __ldg(adj + f);
+        ++my_cand;
+        if (!accept(st, 1, row, w, ws, rot, x0, x1, bc, off, adj, my_probe)) continue;
+        if (kStage) {
+          if (ns < kRowSlots) {
+            const int sl = tid * kRowSlots + ns;
+            sv_row[sl] = tid;
+            sv_x[2 * sl] = x0;
+            sv_x[2 * sl + 1] = x1;
+          } else {
+            ovf = true;
+          }
+        }
+        ++ns;
+      }
+    }
+  }
+  if (io.stats) {
+    unsigned long long tc = RedU(tmp.r).Sum((unsigned long long)my_cand);
+    __syncthreads();
+    unsigned long long tp = RedU(tmp.r).Sum((unsigned long long)my_probe);
+    __syncthreads();
+    if (tid == 0) {
+      atomicAdd(io.stats, tc);
+      atomicAdd(io.stats + 1, tp);
+    }
+  }
+  if (MODE == kModeCount) {
+    unsigned long long t = RedU(tmp.r).Sum((unsigned long long)ns);
+    if (tid == 0) {
+      if (io.block_cnt) io.block_cnt[tile] = t;
+      if (io.total) atomicAdd(io.total, t);
+    }
+    return;
+  }
+  int pos, agg;
+  ScanI(tmp.i).ExclusiveSum(ns, pos, agg);
+  const bool any_ovf = __syncthreads_or(ovf);
+  if (!any_ovf)
+    for (int i = 0; i < ns; ++i) map[pos + i] = tid * kRowSlots + i;
+  if (tid < 32) {
+    const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
+    if (tid == 0) {
+      atomicAdd(io.ctrl + 2, (unsigned long long)agg);
+      const bool fits = !any_ovf && excl + (unsigned long long)agg <= io.cap;
+      if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
+      s_bc = fits ? excl : ~0ull;
+    }
+  }
+  __syncthreads();
+  if (s_bc != ~0ull) flush_rows(rows, sv_row, sv_x, map, w, st.n_new, agg, io.out, (int64_t)s_bc);
+}
+
+size_t rows_smem_bytes(int in_w, bool stage) {
+  size_t b = sizeof(int32_t) * (size_t)kTileRows * row_stride(in_w);
+  if (stage) b += sizeof(int32_t) * (size_t)kTileRows * kRowSlots * 4;
+  return b;
 }
 
 // exclusive prefix over tiles from the look-back status words: excl[t] = inclusive[t-1]
@@ -469,7 +671,7 @@ __global__ void k_status_to_excl(const unsigned long long *__restrict__ status, 
 // Raise the dynamic shared-memory limit of a kernel once per (device, kernel) growth.
 cudaError_t prep(const void *fn, int which, size_t smem) {
   static std::mutex mu;
-  static size_t configured[64][3] = {};
+  static size_t configured[64][6] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -480,10 +682,23 @@ cudaError_t prep(const void *fn, int which, size_t smem) {
   return e;
 }
 
+// Low-degree graphs take the row-serial kernel (count and single-pass launches); re-runs at
+// exact offsets (kModeWrite) and skewed graphs take the candidate-partitioned kernel.
+bool use_row_serial(const DevStep &st, const dm_graph &g) {
+  return st.n_new == 1 ? g.max_deg <= kRowSerialDeg1 : g.max_deg <= kRowSerialDeg2;
+}
+
 template <int MODE>
 cudaError_t launch(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t num_tiles,
                    cudaStream_t s) {
   if (num_tiles <= 0) return cudaSuccess;
+  if (MODE != kModeWrite && use_row_serial(st, g)) {
+    size_t smem = rows_smem_bytes(st.in_w, MODE != kModeCount);
+    cudaError_t e = prep((const void *)k_rows<MODE>, 3 + MODE, smem);
+    if (e != cudaSuccess) return e;
+    k_rows<MODE><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
+    return cudaGetLastError();
+  }
   size_t smem = smem_bytes(st.in_w, MODE != kModeCount);
   cudaError_t e = prep((const void *)k_step<MODE>, MODE, smem);
   if (e != cudaSuccess) return e;

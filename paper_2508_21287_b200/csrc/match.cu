@@ -40,7 +40,7 @@ __global__ void k_iota(uint32_t *p, int64_t n) {
     p[i] = (uint32_t)i;
 }
 
-// keys[i] = table[perm[i]][col]
+// keys[i] = table[perm[i]][col]   (table rows have stride k = row_stride(pattern size))
 __global__ void k_gather_col(const int32_t *__restrict__ table, int k, int col,
                              const uint32_t *__restrict__ perm, uint32_t *__restrict__ keys,
                              int64_t n) {
@@ -53,7 +53,7 @@ __global__ void k_gather_col(const int32_t *__restrict__ table, int k, int col,
 struct ColMap {
   int32_t c[DM_MAX_PATTERN];
 };
-__global__ void k_gather_rows(const int32_t *__restrict__ table, int k, const ColMap cm,
+__global__ void k_gather_rows(const int32_t *__restrict__ table, int k, int ks, const ColMap cm,
                               const uint32_t *__restrict__ perm, int32_t *__restrict__ out,
                               int64_t n) {
   const int64_t total = n * k;
@@ -61,7 +61,7 @@ __global__ void k_gather_rows(const int32_t *__restrict__ table, int k, const Co
        t += (int64_t)gridDim.x * blockDim.x) {
     int64_t i = t / k;
     int p = (int)(t - i * k);
-    out[t] = table[(int64_t)perm[i] * k + cm.c[p]];
+    out[t] = table[(int64_t)perm[i] * ks + cm.c[p]];
   }
 }
 
@@ -205,7 +205,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   const int nsteps = (int)c.plan->steps.size();
   const DevStep &D = c.dsteps[(size_t)si];
   const bool last = si == nsteps - 1;
-  const int W = D.in_w + D.n_new;
+  const int W = row_stride(D.in_w + D.n_new);  // stored (16-byte padded) output row width
   const int64_t tiles = (in_rows + kTileRows - 1) / kTileRows;
   c.st.rows_in[si] += (uint64_t)in_rows;
   c.st.num_chunks++;
@@ -382,7 +382,7 @@ dm_status canonicalize(Ctx &c, int32_t *host_out) {
   CK(tmp.alloc(tb, c.s), "sort temp");
   for (int p = k - 1; p >= 0; --p) {
     const int col = c.plan->pvert_col[(size_t)p];
-    k_gather_col<<<grid_for(n), 256, 0, c.s>>>(c.d_res, k, col, dv.Current(), dk.Current(), n);
+    k_gather_col<<<grid_for(n), 256, 0, c.s>>>(c.d_res, row_stride(k), col, dv.Current(), dk.Current(), n);
     CK(cudaGetLastError(), "gather");
     CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, n, 0, end_bit, c.s), "sort");
     c.st.num_launches += 2;
@@ -391,7 +391,7 @@ dm_status canonicalize(Ctx &c, int32_t *host_out) {
   for (int p = 0; p < k; ++p) cm.c[p] = c.plan->pvert_col[(size_t)p];
   DevBuf<int32_t> outb;
   CK(outb.alloc((size_t)n * k, c.s), "canonical table");
-  k_gather_rows<<<grid_for(n * k), 256, 0, c.s>>>(c.d_res, k, cm, dv.Current(), outb.p, n);
+  k_gather_rows<<<grid_for(n * k), 256, 0, c.s>>>(c.d_res, k, row_stride(k), cm, dv.Current(), outb.p, n);
   CK(cudaGetLastError(), "gather rows");
   c.st.num_launches++;
   c.prof.end(e);
@@ -420,7 +420,10 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   if (opt_in) opt = *opt_in;
   if (!(opt.output & (DM_OUT_COUNT | DM_OUT_TABLE))) return fail(DM_ERR_ARG, "output must request count and/or table");
   Plan plan;
-  dm_status stt = build_plan(k, p_edges, pm, opt.motifs, opt.mode, plan);
+  PlanStats pstats;
+  pstats.n = (double)std::max<int32_t>(g->n, 2);
+  pstats.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
+  dm_status stt = build_plan(k, p_edges, pm, opt.motifs, opt.mode, plan, pstats);
   if (stt != DM_OK) return stt;
   int64_t sb = std::max<int64_t>(0, opt.seed_begin);
   int64_t se = opt.seed_end < 0 ? g->n : std::min<int64_t>(opt.seed_end, g->n);

@@ -23,6 +23,7 @@
 // pushdown that leaves the final table unchanged).  Slices whose vertices are all
 // placed therefore need no step of their own (their joins are pure closing-edge probes).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <sstream>
@@ -89,10 +90,82 @@ bool first_match(const Pat &P, const MotifT &M, const std::vector<char> &alive,
   return true;
 }
 
+
+// Compile a slice execution order into kernel steps.  Each slice contributes its unplaced
+// vertices as one step (ordered so each has a placed pattern neighbour); every pattern edge
+// between a new vertex and a placed vertex is enforced when the later endpoint is placed.
+dm_status compile_order(const Pat &P, int mode, const std::vector<int> &order, int first,
+                        Plan &plan) {
+  const int k = P.k;
+  plan.steps.clear();
+  plan.col_pvert.clear();
+  plan.pvert_col.assign(k, -1);
+  plan.order = order;
+  auto place = [&](int pv) {
+    plan.pvert_col[pv] = (int)plan.col_pvert.size();
+    plan.col_pvert.push_back(pv);
+  };
+  plan.first_vertex = first;
+  place(first);
+  for (int si : order) {
+    const Slice &s = plan.slices[(size_t)si];
+    std::vector<int> fresh;
+    for (int i = 0; i < s.nv; ++i)
+      if (plan.pvert_col[s.v[i]] < 0) fresh.push_back(s.v[i]);
+    if (fresh.empty()) continue;  // pure closing-edge slice: enforced by pushdown
+    Step st;
+    st.slice = si;
+    st.in_w = (int)plan.col_pvert.size();
+    while (!fresh.empty()) {
+      size_t pick = fresh.size();
+      for (size_t j = 0; j < fresh.size() && pick == fresh.size(); ++j)
+        for (int u = 0; u < k; ++u)
+          if (P.adj[fresh[j]][u] && plan.pvert_col[u] >= 0) { pick = j; break; }
+      if (pick == fresh.size()) return DM_ERR_ARG;
+      const int v = fresh[pick];
+      fresh.erase(fresh.begin() + (long)pick);
+      if (st.n_new == 2) return DM_ERR_ARG;
+      StepVertex sv;
+      sv.pvert = v;
+      for (int c = 0; c < (int)plan.col_pvert.size(); ++c) {
+        const int u = plan.col_pvert[(size_t)c];
+        if (P.adj[v][u]) sv.nbr[sv.n_nbr++] = c;
+        else if (mode == DM_INDUCED) sv.non[sv.n_non++] = c;
+      }
+      st.nv[st.n_new++] = sv;
+      place(v);
+    }
+    plan.steps.push_back(st);
+  }
+  return (int)plan.col_pvert.size() == k ? DM_OK : DM_ERR_ARG;
+}
+
+// Frontier-size model: level sizes grow by d_avg per new vertex and shrink by the edge
+// probability p = d_avg/(n-1) per extra join key; cost = bytes of every materialized level
+// (written + read once) + one byte-equivalent per candidate per compared column.
+double estimate_cost(const Plan &plan, const PlanStats &st) {
+  const double n = std::max(2.0, st.n), d = std::max(1.0, st.avg_degree);
+  const double p = std::min(1.0, d / (n - 1.0));
+  double rows = n, cost = 0.0;
+  for (size_t i = 0; i < plan.steps.size(); ++i) {
+    const Step &s = plan.steps[i];
+    double cand = 0.0;
+    for (int j = 0; j < s.n_new; ++j) {
+      cand += rows * d;
+      rows *= d * std::pow(p, s.nv[j].n_nbr - 1);
+    }
+    cost += cand * (s.in_w + 1);
+    const int wout = s.in_w + s.n_new;
+    if (i + 1 < plan.steps.size()) cost += 2.0 * 4.0 * rows * ((wout + 3) & ~3);
+  }
+  return cost;
+}
+
 }  // namespace
 
+
 dm_status build_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs, int32_t mode,
-                     Plan &out) {
+                     Plan &out, const PlanStats &stats) {
   if (k < 1) return fail(DM_ERR_ARG, "pattern must have k >= 1 vertices");
   if (k > DM_MAX_PATTERN) return fail(DM_ERR_UNSUPPORTED, "pattern larger than DM_MAX_PATTERN");
   if (pm < 0 || (pm > 0 && !p_edges)) return fail(DM_ERR_ARG, "bad pattern edge list");
@@ -166,54 +239,52 @@ dm_status build_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t moti
   }
 
   // ------------------------------------------------------------ join program
-  plan.pvert_col.assign(k, -1);
-  auto place = [&](int pv) {
-    plan.pvert_col[pv] = (int)plan.col_pvert.size();
-    plan.col_pvert.push_back(pv);
-  };
   if (plan.slices.empty()) {  // k == 1: the result is the implicit vertex table
     plan.first_vertex = 0;
-    place(0);
-  } else {
-    plan.first_vertex = plan.slices[0].v[0];
-    place(plan.first_vertex);
+    plan.col_pvert = {0};
+    plan.pvert_col = {0};
+    out = std::move(plan);
+    return DM_OK;
   }
-  for (size_t si = 0; si < plan.slices.size(); ++si) {
-    const Slice &s = plan.slices[si];
-    std::vector<int> fresh;
-    for (int i = 0; i < s.nv; ++i)
-      if (plan.pvert_col[s.v[i]] < 0) fresh.push_back(s.v[i]);
-    if (fresh.empty()) continue;  // pure closing-edge slice: enforced by pushdown
-    Step st;
-    st.slice = (int)si;
-    st.in_w = (int)plan.col_pvert.size();
-    // order the new vertices so that each has an already-placed pattern neighbour
-    std::vector<int> ordered;
-    while (!fresh.empty()) {
-      size_t pick = fresh.size();
-      for (size_t j = 0; j < fresh.size() && pick == fresh.size(); ++j)
-        for (int u = 0; u < k; ++u)
-          if (P.adj[fresh[j]][u] && plan.pvert_col[u] >= 0) { pick = j; break; }
-      if (pick == fresh.size()) return fail(DM_ERR_ARG, "internal: slice not connected to placed vertices");
-      int v = fresh[pick];
-      fresh.erase(fresh.begin() + (long)pick);
-      StepVertex sv;
-      sv.pvert = v;
-      for (int c = 0; c < (int)plan.col_pvert.size(); ++c) {
-        int u = plan.col_pvert[c];
-        if (P.adj[v][u]) sv.nbr[sv.n_nbr++] = c;
-        else if (mode == DM_INDUCED) sv.non[sv.n_non++] = c;
+  // Candidate execution orders: every (seed slice, first vertex) pair, then greedily the
+  // lowest-index slice that shares a vertex with the placed ones (left-deep; the paper's own
+  // order is the candidate seeded by slice 0, and "the join order can also be
+  // reversed").  The cheapest order under a simple frontier-size model wins.
+  const int ns = (int)plan.slices.size();
+  double best_cost = -1.0;
+  Plan best;
+  for (int seed = 0; seed < ns; ++seed) {
+    for (int fv = 0; fv < plan.slices[seed].nv; ++fv) {
+      std::vector<int> order{seed};
+      std::vector<char> used(ns, 0), placed(k, 0);
+      used[seed] = 1;
+      for (int i = 0; i < plan.slices[seed].nv; ++i) placed[plan.slices[seed].v[i]] = 1;
+      while ((int)order.size() < ns) {
+        int pick = -1;
+        for (int si = 0; si < ns && pick < 0; ++si) {
+          if (used[si]) continue;
+          for (int i = 0; i < plan.slices[si].nv; ++i)
+            if (placed[plan.slices[si].v[i]]) { pick = si; break; }
+        }
+        if (pick < 0) break;
+        used[pick] = 1;
+        order.push_back(pick);
+        for (int i = 0; i < plan.slices[pick].nv; ++i) placed[plan.slices[pick].v[i]] = 1;
       }
-      st.nv[st.n_new++] = sv;
-      place(v);
-      ordered.push_back(v);
+      if ((int)order.size() != ns) continue;
+      Plan cand = plan;
+      if (compile_order(P, mode, order, plan.slices[seed].v[fv], cand) != DM_OK) continue;
+      const double cost = estimate_cost(cand, stats);
+      if (best_cost < 0 || cost < best_cost - 1e-9 * best_cost) {
+        best_cost = cost;
+        best = std::move(cand);
+      }
     }
-    if (st.n_new > 2) return fail(DM_ERR_ARG, "internal: step adds more than 2 vertices");
-    plan.steps.push_back(st);
   }
-  if ((int)plan.col_pvert.size() != k) return fail(DM_ERR_ARG, "internal: not all pattern vertices placed");
-  if ((int)plan.steps.size() > DM_MAX_STEPS) return fail(DM_ERR_UNSUPPORTED, "too many join steps");
-  out = std::move(plan);
+  if (best_cost < 0) return fail(DM_ERR_ARG, "internal: no valid join order");
+  if ((int)best.col_pvert.size() != k) return fail(DM_ERR_ARG, "internal: not all pattern vertices placed");
+  if ((int)best.steps.size() > DM_MAX_STEPS) return fail(DM_ERR_UNSUPPORTED, "too many join steps");
+  out = std::move(best);
   return DM_OK;
 }
 
