@@ -44,9 +44,10 @@ struct DeviceGuard {
 constexpr int kStepThreads = 256;   // threads per CTA
 constexpr int kTileRows = 256;      // frontier rows per CTA tile
 constexpr int kSurvBuf = 1024;      // survivors staged in shared memory per CTA
-constexpr int kRowSlots = 8;        // row-serial kernel: survivor slots per frontier row
+constexpr int kRowSlotsMax = 8;     // row-serial kernel: max survivor slots per frontier row
 constexpr int kRowSerialDeg1 = 16;  // row-serial kernel for 1-vertex steps if max degree <= 16
-constexpr int kRowSerialDeg2 = 6;   //   ... and for 2-vertex steps if max degree <= 6
+constexpr int kRowSerialDeg2 = 4;   //   ... and for 2-vertex steps if max degree <= 4
+constexpr int kAccSlots = 64;       // counters are spread over 64 slots (atomic contention)
 constexpr int kModeCount = 0;       // join-step kernel launch modes (see extend.cu)
 constexpr int kModeWrite = 1;
 constexpr int kModeSingle = 2;
@@ -74,12 +75,13 @@ struct StepIO {
   const uint64_t *block_off;  // write pass: exclusive prefix of survivors per tile (global)
   uint64_t out_base;          // write pass: block_off value that maps to out row 0
   uint64_t *block_cnt;        // count pass: survivors per tile (nullptr -> only total)
-  unsigned long long *total;  // count pass: += survivors (nullptr -> skip)
-  unsigned long long *stats;  // [0] += candidates, [1] += probes (nullptr -> skip)
+  unsigned long long *total;  // count pass: [tile % kAccSlots] += survivors (nullptr -> skip)
+  unsigned long long *stats;  // [slot] += candidates, [kAccSlots + slot] += probes (or nullptr)
   unsigned long long *status; // single pass: look-back status word per tile (zeroed)
   unsigned long long *ctrl;   // single pass: [0] tile counter (0), [1] first unwritten tile
                               //   (init = #tiles), [2] += survivors
   uint64_t cap;               // single pass: output capacity in rows
+  int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
 };
 
 size_t step_smem_bytes(int in_w, bool write_pass);

@@ -70,27 +70,35 @@ __device__ __forceinline__ bool has_edge(const int64_t *__restrict__ off,
   return lo < end && __ldg(adj + lo) == key;
 }
 
-// x in row?  The row is 16-byte aligned and padded with -1 to ws words (a multiple of 4),
-// so the all-distinct test is ws/4 LDS.128 + compares, branch-free.  Rows sit at stride ws in
-// shared memory; when ws/4 is even, consecutive rows would start in the same bank group, so
-// each row starts its scan at chunk `rot` (= row index mod ws/4) -> conflict-free LDS.128.
-__device__ __forceinline__ bool in_row(const int32_t *row, int ws, int rot, int32_t x) {
+// x in row?  The row is 16-byte aligned and padded with -1 to a multiple of 4 words, so the
+// all-distinct test is ws/4 LDS.128 + predicated compares, branch-free.  In shared memory the
+// rows sit at an odd number of 16-byte chunks (smem_stride), so the LDS.128 of 8 consecutive
+// rows hit 8 distinct bank groups (conflict-free).
+__device__ __forceinline__ bool in_row(const int32_t *row, int ws, int32_t x) {
   const int4 *r4 = reinterpret_cast<const int4 *>(row);
   const int nq = ws >> 2;
   bool hit = false;
-  int idx = rot;
 #pragma unroll 4
   for (int q = 0; q < nq; ++q) {
-    const int4 v = r4[idx];
+    const int4 v = r4[q];
     hit |= (v.x == x) | (v.y == x) | (v.z == x) | (v.w == x);
-    idx = idx + 1 == nq ? 0 : idx + 1;
   }
   return hit;
 }
 
-__device__ __forceinline__ int row_rot(int r, int ws) {
-  const int nq = ws >> 2;
-  return (nq & 1) ? 0 : r % nq;
+// shared-memory row stride (words): the global stride padded to an odd number of int4 chunks
+__host__ __device__ inline int smem_stride(int w) {
+  const int ws = row_stride(w);
+  return ((ws >> 2) & 1) ? ws : ws + 4;
+}
+
+// cp.async 16-byte copy global -> shared (LDGSTS), for tiles whose smem stride differs
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // ---- TMA 1-D bulk copy global -> shared, completion tracked by an mbarrier (sm_90+ / sm_100a)
@@ -124,6 +132,65 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
   }
 }
 
+
+// Tile of nrows frontier rows -> shared memory at stride ss.  Contiguous case (ss == ws): one
+// TMA bulk copy completing on an mbarrier; padded case: 16-byte cp.async per chunk, one warp
+// per row.  Implicit seed: row r = vertex seed_base + r0 + r.  Ends with a CTA barrier.
+__device__ __forceinline__ void load_tile(int32_t *rows, int ss, int ws, const StepIO &io,
+                                          int64_t r0, int nrows, uint64_t *bar) {
+  const int tid = threadIdx.x;
+  if (!io.in) {
+    for (int r = tid; r < nrows; r += kStepThreads) {
+      int4 *d = reinterpret_cast<int4 *>(rows + r * ss);
+      d[0] = make_int4((int32_t)(io.seed_base + r0 + r), -1, -1, -1);
+    }
+    __syncthreads();
+    return;
+  }
+  const int32_t *src = io.in + r0 * ws;
+  if (ss == ws) {
+    if (tid == 0) {
+      mbar_init(bar, 1);
+      const unsigned bytes = (unsigned)(nrows * ws) * 4u;
+      mbar_expect_tx(bar, bytes);
+      tma_bulk_g2s(rows, src, bytes, bar);
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    mbar_wait(bar, 0);
+    return;
+  }
+  const int nq = ws >> 2;
+  const int lane = tid & 31, warp = tid >> 5;
+  int lpr = 1;
+  while (lpr < nq) lpr <<= 1;
+  const int rpi = 32 / lpr, q = lane & (lpr - 1), sub = lane / lpr;
+  if (q < nq)
+    for (int r = warp * rpi + sub; r < nrows; r += (kStepThreads / 32) * rpi)
+      cp_async16(rows + r * ss + 4 * q, src + (int64_t)r * ws + 4 * q);
+  cp_async_wait_all();
+  __syncthreads();
+}
+
+
+// CTA-wide sum of three counters (result valid in thread 0)
+__device__ __forceinline__ void block_sum3(unsigned long long v[3]) {
+  __shared__ unsigned long long part[kStepThreads / 32][3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  if (lane == 0)
+    for (int i = 0; i < 3; ++i) part[warp][i] = v[i];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < 3; ++i) {
+      unsigned long long t = 0;
+      for (int k = 0; k < kStepThreads / 32; ++k) t += part[k][i];
+      v[i] = t;
+    }
+}
+
 // value of column c of the row being built (c == w -> first new vertex)
 __device__ __forceinline__ int32_t colval(const int32_t *row, int w, int c, int32_t x0) {
   return c < w ? row[c] : x0;
@@ -132,10 +199,10 @@ __device__ __forceinline__ int32_t colval(const int32_t *row, int w, int c, int3
 // Filters for new vertex j with candidate value x (anchor column `acol` is satisfied by
 // construction): all-distinct, closing-edge probes, induced non-edge probes.
 __device__ __forceinline__ bool accept(const DevStep &st, int j, const int32_t *row, int w, int ws,
-                                       int rot, int32_t x0, int32_t x, int acol,
+                                       int32_t x0, int32_t x, int acol,
                                        const int64_t *__restrict__ off,
                                        const int32_t *__restrict__ adj, uint32_t &probes) {
-  if (in_row(row, ws, rot, x)) return false;
+  if (in_row(row, ws, x)) return false;
   if (j == 1 && x == x0) return false;
   for (int t = 0; t < st.n_nbr[j]; ++t) {
     int c = st.nbr[j][t];
@@ -188,7 +255,7 @@ struct SmemLayout {
 };
 
 __host__ __device__ inline size_t smem_bytes(int in_w, bool stage) {
-  size_t b = align16(sizeof(int32_t) * (size_t)kTileRows * row_stride(in_w));
+  size_t b = align16(sizeof(int32_t) * (size_t)kTileRows * smem_stride(in_w));
   b += align16(sizeof(long long) * (kTileRows + 1));
   b += align16(sizeof(long long) * kTileRows);
   b += align16(sizeof(int32_t) * kTileRows);
@@ -208,7 +275,7 @@ __device__ inline SmemLayout carve(unsigned char *base, int in_w, bool stage) {
     o += align16(bytes);
     return p;
   };
-  L.rows = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * (size_t)kTileRows * row_stride(in_w)));
+  L.rows = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * (size_t)kTileRows * smem_stride(in_w)));
   L.pref = reinterpret_cast<long long *>(take(sizeof(long long) * (kTileRows + 1)));
   L.abeg = reinterpret_cast<long long *>(take(sizeof(long long) * kTileRows));
   L.acol = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * kTileRows));
@@ -231,11 +298,13 @@ __device__ inline SmemLayout carve(unsigned char *base, int in_w, bool stage) {
 // A row is Wp/4 int4 chunks; lpr lanes (power of two >= Wp/4) cover one row, so one warp
 // store instruction writes 32/lpr consecutive rows = a contiguous, 16-byte aligned span.
 // The new vertices are patched into the chunk that holds columns w, w+1.
+// map == nullptr: staged entry o is (sv_row[o], sv_x[2o], sv_x[2o+1]); otherwise map[o] =
+// (row << 4 | i) names slot row*S + i of the per-row slots (row-serial kernel).
 __device__ __forceinline__ void flush_rows(const int32_t *rows, const int32_t *sv_row,
-                                           const int32_t *sv_x, const int32_t *map, int w,
+                                           const int32_t *sv_x, const int32_t *map, int S, int w,
                                            int n_new, int fill, int32_t *__restrict__ out,
                                            int64_t base) {
-  const int ws = row_stride(w), Wp = row_stride(w + n_new);
+  const int ws = row_stride(w), ss = smem_stride(w), Wp = row_stride(w + n_new);
   const int nq = Wp >> 2, nqs = ws >> 2;
   int lpr = 1;
   while (lpr < nq) lpr <<= 1;
@@ -249,9 +318,16 @@ __device__ __forceinline__ void flush_rows(const int32_t *rows, const int32_t *s
   const bool has0 = k0 >= 0 && k0 < 4, has1 = n_new == 2 && k1 >= 0 && k1 < 4;
   int4 *out4 = reinterpret_cast<int4 *>(out);
   for (int o = warp * rpi + sub; o < fill; o += nwarps * rpi) {
-    const int s = map ? map[o] : o;
-    int4 v = q < nqs ? reinterpret_cast<const int4 *>(rows + sv_row[s] * ws)[q]
-                     : make_int4(-1, -1, -1, -1);
+    int s, r;
+    if (map) {
+      const int m = map[o];
+      r = m >> 4;
+      s = r * S + (m & 15);
+    } else {
+      s = o;
+      r = sv_row[o];
+    }
+    int4 v = q < nqs ? reinterpret_cast<const int4 *>(rows + r * ss)[q] : make_int4(-1, -1, -1, -1);
     if (has0) {
       const int32_t x0 = sv_x[2 * s];
       v.x = k0 == 0 ? x0 : v.x;
@@ -327,6 +403,7 @@ __global__ void __launch_bounds__(kStepThreads)
 
   const int w = st.in_w;
   const int ws = row_stride(w);
+  const int ss = smem_stride(w);
   const int tid = threadIdx.x;
   int64_t tile;
   if (MODE == kModeSingle) {
@@ -341,28 +418,15 @@ __global__ void __launch_bounds__(kStepThreads)
   const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
   SmemLayout L = carve(smem_raw, w, kStage);
 
-  // ---- 1. tile -> shared memory: one TMA bulk copy (rows are 16-byte strided)
-  if (io.in) {
-    if (tid == 0) {
-      mbar_init(&s_bar, 1);
-      const unsigned bytes = (unsigned)(nrows * ws) * 4u;
-      mbar_expect_tx(&s_bar, bytes);
-      tma_bulk_g2s(L.rows, io.in + r0 * ws, bytes, &s_bar);
-    }
-    __syncthreads();  // barrier initialised before anyone waits on it
-    mbar_wait(&s_bar, 0);
-  } else {  // implicit seed table: row r = vertex seed_base + r0 + r
-    for (int r = tid; r < nrows; r += kStepThreads)
-      reinterpret_cast<int4 *>(L.rows)[r] = make_int4((int32_t)(io.seed_base + r0 + r), -1, -1, -1);
-    __syncthreads();
-  }
+  // ---- 1. tile -> shared memory
+  load_tile(L.rows, ss, ws, io, r0, nrows, &s_bar);
 
   // ---- 2. per-row join key for the first new vertex; tile candidate space
   long long cnt = 0;
   if (tid < nrows) {
     int32_t av;
     int64_t ad;
-    L.acol[tid] = pick_anchor(st, 0, L.rows + tid * ws, w, 0, off, av, ad);
+    L.acol[tid] = pick_anchor(st, 0, L.rows + tid * ss, w, 0, off, av, ad);
     L.abeg[tid] = __ldg(off + av);
     cnt = ad;
   }
@@ -390,7 +454,7 @@ __global__ void __launch_bounds__(kStepThreads)
     ScanI(tmp.i).ExclusiveSum(s ? 1 : 0, pos, tot);
     if (MODE == kModeWrite && fill + tot > kSurvBuf) {
       __syncthreads();
-      flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, w, st.n_new, fill, io.out, base);
+      flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, 0, w, st.n_new, fill, io.out, base);
       __syncthreads();
       base += fill;
       fill = 0;
@@ -434,7 +498,7 @@ __global__ void __launch_bounds__(kStepThreads)
     if (j < C0) {
       x0 = __ldg(adj + L.abeg[r] + (j - L.pref[r]));
       ++my_cand;
-      ok = accept(st, 0, L.rows + r * ws, w, ws, row_rot(r, ws), 0, x0, L.acol[r], off, adj, my_probe);
+      ok = accept(st, 0, L.rows + r * ss, w, ws, 0, x0, L.acol[r], off, adj, my_probe);
     }
     if (st.n_new == 1) {
       emit(ok, r, x0, -1);
@@ -445,7 +509,7 @@ __global__ void __launch_bounds__(kStepThreads)
     if (ok) {
       int32_t av;
       int64_t ad;
-      L.aacol[tid] = pick_anchor(st, 1, L.rows + r * ws, w, x0, off, av, ad);
+      L.aacol[tid] = pick_anchor(st, 1, L.rows + r * ss, w, x0, off, av, ad);
       L.aabeg[tid] = __ldg(off + av);
       L.ar[tid] = r;
       L.ax0[tid] = x0;
@@ -467,7 +531,7 @@ __global__ void __launch_bounds__(kStepThreads)
         xa = L.ax0[t];
         x1 = __ldg(adj + L.aabeg[t] + (q - L.apref[t]));
         ++my_cand;
-        ok1 = accept(st, 1, L.rows + ra * ws, w, ws, row_rot(ra, ws), xa, x1, L.aacol[t], off, adj, my_probe);
+        ok1 = accept(st, 1, L.rows + ra * ss, w, ws, xa, x1, L.aacol[t], off, adj, my_probe);
       }
       emit(ok1, ra, xa, x1);
     }
@@ -477,27 +541,25 @@ __global__ void __launch_bounds__(kStepThreads)
   // ---- 4. finish
   if (MODE == kModeWrite) {
     __syncthreads();
-    flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, w, st.n_new, fill, io.out, base);
+    flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, 0, w, st.n_new, fill, io.out, base);
     return;
   }
-  if (io.stats) {
-    unsigned long long tc = RedU(tmp.r).Sum((unsigned long long)my_cand);
-    __syncthreads();
-    unsigned long long tp = RedU(tmp.r).Sum((unsigned long long)my_probe);
-    __syncthreads();
+  if (io.stats || MODE == kModeCount) {
+    unsigned long long v3[3] = {my_cand, my_probe, my_surv};
+    block_sum3(v3);
     if (tid == 0) {
-      atomicAdd(io.stats, tc);
-      atomicAdd(io.stats + 1, tp);
+      const int slot = (int)(tile & (kAccSlots - 1));
+      if (io.stats) {
+        atomicAdd(io.stats + slot, v3[0]);
+        atomicAdd(io.stats + kAccSlots + slot, v3[1]);
+      }
+      if (MODE == kModeCount) {
+        if (io.block_cnt) io.block_cnt[tile] = v3[2];
+        if (io.total && v3[2]) atomicAdd(io.total + slot, v3[2]);
+      }
     }
   }
-  if (MODE == kModeCount) {
-    unsigned long long t = RedU(tmp.r).Sum(my_surv);
-    if (tid == 0) {
-      if (io.block_cnt) io.block_cnt[tile] = t;
-      if (io.total) atomicAdd(io.total, t);
-    }
-    return;
-  }
+  if (MODE == kModeCount) return;
   // kModeSingle: decoupled look-back for the tile's exclusive prefix, then write
   if (tid < 32) {
     const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
@@ -509,7 +571,7 @@ __global__ void __launch_bounds__(kStepThreads)
     }
   }
   __syncthreads();
-  if (s_bc != ~0ull) flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, w, st.n_new, fill, io.out, (int64_t)s_bc);
+  if (s_bc != ~0ull) flush_rows(L.rows, L.sv_row, L.sv_x, nullptr, 0, w, st.n_new, fill, io.out, (int64_t)s_bc);
 }
 
 
@@ -526,18 +588,16 @@ __global__ void __launch_bounds__(kStepThreads)
            const int32_t *__restrict__ adj) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typedef cub::BlockScan<int, kStepThreads> ScanI;
-  typedef cub::BlockReduce<unsigned long long, kStepThreads> RedU;
-  __shared__ union {
-    typename ScanI::TempStorage i;
-    typename RedU::TempStorage r;
-  } tmp;
+  __shared__ typename ScanI::TempStorage tmp;
   __shared__ unsigned long long s_bc;
   __shared__ __align__(8) uint64_t s_bar;
   constexpr bool kStage = MODE != kModeCount;
 
   const int w = st.in_w;
   const int ws = row_stride(w);
-  const int tid = threadIdx.x;
+  const int ss = smem_stride(w);
+  const int S = io.slots;
+  const int tid = threadIdx.x, lane = tid & 31;
   int64_t tile;
   if (MODE == kModeSingle) {
     if (tid == 0) s_bc = atomicAdd(io.ctrl + 0, 1ull);
@@ -550,31 +610,16 @@ __global__ void __launch_bounds__(kStepThreads)
   if (r0 >= io.in_rows) return;
   const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
   int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
-  int32_t *sv_row = rows + kTileRows * ws;              // [kTileRows * kRowSlots]
-  int32_t *sv_x = sv_row + kTileRows * kRowSlots;       // [kTileRows * kRowSlots][2]
-  int32_t *map = sv_x + 2 * kTileRows * kRowSlots;      // [kTileRows * kRowSlots]
+  int32_t *sv_x = rows + kTileRows * ss;         // [kTileRows * S][2]
+  int32_t *map = sv_x + 2 * kTileRows * S;       // [kTileRows * S]
 
-  if (io.in) {
-    if (tid == 0) {
-      mbar_init(&s_bar, 1);
-      const unsigned bytes = (unsigned)(nrows * ws) * 4u;
-      mbar_expect_tx(&s_bar, bytes);
-      tma_bulk_g2s(rows, io.in + r0 * ws, bytes, &s_bar);
-    }
-    __syncthreads();
-    mbar_wait(&s_bar, 0);
-  } else {
-    for (int r = tid; r < nrows; r += kStepThreads)
-      reinterpret_cast<int4 *>(rows)[r] = make_int4((int32_t)(io.seed_base + r0 + r), -1, -1, -1);
-    __syncthreads();
-  }
+  load_tile(rows, ss, ws, io, r0, nrows, &s_bar);
 
   int ns = 0;
   bool ovf = false;
   uint32_t my_cand = 0, my_probe = 0;
   if (tid < nrows) {
-    const int32_t *row = rows + tid * ws;
-    const int rot = row_rot(tid, ws);
+    const int32_t *row = rows + tid * ss;
     int32_t av;
     int64_t ad;
     const int ac = pick_anchor(st, 0, row, w, 0, off, av, ad);
@@ -582,16 +627,11 @@ __global__ void __launch_bounds__(kStepThreads)
     for (int64_t e = e0; e < e0 + ad; ++e) {
       const int32_t x0 = __ldg(adj + e);
       ++my_cand;
-      if (!accept(st, 0, row, w, ws, rot, 0, x0, ac, off, adj, my_probe)) continue;
+      if (!accept(st, 0, row, w, ws, 0, x0, ac, off, adj, my_probe)) continue;
       if (st.n_new == 1) {
         if (kStage) {
-          if (ns < kRowSlots) {
-            const int sl = tid * kRowSlots + ns;
-            sv_row[sl] = tid;
-            sv_x[2 * sl] = x0;
-          } else {
-            ovf = true;
-          }
+          if (ns < S) sv_x[2 * (tid * S + ns)] = x0;
+          else ovf = true;
         }
         ++ns;
         continue;
@@ -603,11 +643,10 @@ __global__ void __launch_bounds__(kStepThreads)
       for (int64_t f = f0; f < f0 + bd; ++f) {
         const int32_t x1 = __ldg(adj + f);
         ++my_cand;
-        if (!accept(st, 1, row, w, ws, rot, x0, x1, bc, off, adj, my_probe)) continue;
+        if (!accept(st, 1, row, w, ws, x0, x1, bc, off, adj, my_probe)) continue;
         if (kStage) {
-          if (ns < kRowSlots) {
-            const int sl = tid * kRowSlots + ns;
-            sv_row[sl] = tid;
+          if (ns < S) {
+            const int sl = tid * S + ns;
             sv_x[2 * sl] = x0;
             sv_x[2 * sl + 1] = x1;
           } else {
@@ -618,29 +657,28 @@ __global__ void __launch_bounds__(kStepThreads)
       }
     }
   }
-  if (io.stats) {
-    unsigned long long tc = RedU(tmp.r).Sum((unsigned long long)my_cand);
-    __syncthreads();
-    unsigned long long tp = RedU(tmp.r).Sum((unsigned long long)my_probe);
-    __syncthreads();
+  // statistics and count-mode totals: CTA reduction, one atomic per CTA on slot tile % 64
+  if (io.stats || MODE == kModeCount) {
+    unsigned long long v3[3] = {my_cand, my_probe, (unsigned long long)ns};
+    block_sum3(v3);
     if (tid == 0) {
-      atomicAdd(io.stats, tc);
-      atomicAdd(io.stats + 1, tp);
+      const int slot = (int)(tile & (kAccSlots - 1));
+      if (io.stats) {
+        atomicAdd(io.stats + slot, v3[0]);
+        atomicAdd(io.stats + kAccSlots + slot, v3[1]);
+      }
+      if (MODE == kModeCount) {
+        if (io.block_cnt) io.block_cnt[tile] = v3[2];
+        if (io.total && v3[2]) atomicAdd(io.total + slot, v3[2]);
+      }
     }
   }
-  if (MODE == kModeCount) {
-    unsigned long long t = RedU(tmp.r).Sum((unsigned long long)ns);
-    if (tid == 0) {
-      if (io.block_cnt) io.block_cnt[tile] = t;
-      if (io.total) atomicAdd(io.total, t);
-    }
-    return;
-  }
+  if (MODE == kModeCount) return;
   int pos, agg;
-  ScanI(tmp.i).ExclusiveSum(ns, pos, agg);
+  ScanI(tmp).ExclusiveSum(ns, pos, agg);
   const bool any_ovf = __syncthreads_or(ovf);
   if (!any_ovf)
-    for (int i = 0; i < ns; ++i) map[pos + i] = tid * kRowSlots + i;
+    for (int i = 0; i < ns; ++i) map[pos + i] = (tid << 4) | i;
   if (tid < 32) {
     const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
     if (tid == 0) {
@@ -651,13 +689,20 @@ __global__ void __launch_bounds__(kStepThreads)
     }
   }
   __syncthreads();
-  if (s_bc != ~0ull) flush_rows(rows, sv_row, sv_x, map, w, st.n_new, agg, io.out, (int64_t)s_bc);
+  if (s_bc != ~0ull) flush_rows(rows, nullptr, sv_x, map, S, w, st.n_new, agg, io.out, (int64_t)s_bc);
 }
 
-size_t rows_smem_bytes(int in_w, bool stage) {
-  size_t b = sizeof(int32_t) * (size_t)kTileRows * row_stride(in_w);
-  if (stage) b += sizeof(int32_t) * (size_t)kTileRows * kRowSlots * 4;
+size_t rows_smem_bytes(int in_w, bool stage, int slots) {
+  size_t b = sizeof(int32_t) * (size_t)kTileRows * smem_stride(in_w);
+  if (stage) b += sizeof(int32_t) * (size_t)kTileRows * slots * 3;
   return b;
+}
+
+// survivor slots per row for the row-serial kernel: min(max_degree^n_new, kRowSlotsMax)
+int row_slots(const DevStep &st, const dm_graph &g) {
+  int64_t d = g.max_deg < 1 ? 1 : g.max_deg;
+  int64_t s = st.n_new == 1 ? d : d * d;
+  return (int)(s < kRowSlotsMax ? s : kRowSlotsMax);
 }
 
 // exclusive prefix over tiles from the look-back status words: excl[t] = inclusive[t-1]
@@ -693,10 +738,12 @@ cudaError_t launch(const DevStep &st, const StepIO &io, const dm_graph &g, int64
                    cudaStream_t s) {
   if (num_tiles <= 0) return cudaSuccess;
   if (MODE != kModeWrite && use_row_serial(st, g)) {
-    size_t smem = rows_smem_bytes(st.in_w, MODE != kModeCount);
+    StepIO io2 = io;
+    io2.slots = row_slots(st, g);
+    size_t smem = rows_smem_bytes(st.in_w, MODE != kModeCount, io2.slots);
     cudaError_t e = prep((const void *)k_rows<MODE>, 3 + MODE, smem);
     if (e != cudaSuccess) return e;
-    k_rows<MODE><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
+    k_rows<MODE><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);
     return cudaGetLastError();
   }
   size_t smem = smem_bytes(st.in_w, MODE != kModeCount);

@@ -127,7 +127,8 @@ struct Ctx {
   uint64_t live = 0;        // bytes of frontier buffers currently held by the recursion
   uint64_t row_budget = 0;
   std::vector<DevStep> dsteps;
-  unsigned long long *d_acc = nullptr;  // [0] count-mode total, [1+2i] C_i, [2+2i] Q_i
+  unsigned long long *d_acc = nullptr;  // [slots] count-mode total, then per step i:
+                                        //   [C_i slots][Q_i slots] (kAccSlots each)
   int32_t *d_res = nullptr;             // table mode: rows in column (match) order
   uint64_t res_rows = 0, res_cap = 0;
   std::vector<double> ratio;            // observed output/input rows per step (capacity estimate)
@@ -215,7 +216,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   io.in_rows = in_rows;
   io.seed_base = seed_base;
   io.block_begin = 0;
-  io.stats = c.d_acc + 1 + 2 * si;
+  io.stats = c.d_acc + kAccSlots + 2 * kAccSlots * si;
 
   if (last && !c.table) {  // count-only last step: reduce, never materialize
     io.total = c.d_acc;
@@ -478,7 +479,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     }
   } rg{res};
 
-  const int nacc = 1 + 2 * (int)plan.steps.size();
+  const int nacc = kAccSlots * (1 + 2 * (int)plan.steps.size());
   CK(cudaMallocAsync((void **)&c.d_acc, sizeof(unsigned long long) * nacc, c.s), "accumulators");
   struct AccGuard {
     Ctx &c;
@@ -519,12 +520,17 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   CK(cudaMemcpyAsync(acc.data(), c.d_acc, sizeof(unsigned long long) * nacc, cudaMemcpyDeviceToHost, c.s),
      "D2H accumulators");
   CK(cudaStreamSynchronize(c.s), "sync");
-  if (!plan.steps.empty() && !c.table) count = acc[0];
+  auto slot_sum = [&](size_t base) {
+    unsigned long long t = 0;
+    for (int i = 0; i < kAccSlots; ++i) t += acc[base + (size_t)i];
+    return t;
+  };
+  if (!plan.steps.empty() && !c.table) count = slot_sum(0);
   if (!plan.steps.empty() && !c.table) c.st.rows_out[plan.steps.size() - 1] = count;
   c.prof.finish(c.st);
   for (size_t i = 0; i < plan.steps.size(); ++i) {
-    c.st.candidates[i] = acc[1 + 2 * i];
-    c.st.probes[i] = acc[2 + 2 * i];
+    c.st.candidates[i] = slot_sum(kAccSlots + 2 * kAccSlots * i);
+    c.st.probes[i] = slot_sum(2 * kAccSlots + 2 * kAccSlots * i);
     const bool lastc = (i + 1 == plan.steps.size()) && !c.table;
     const double win = (i == 0) ? 0.0 : (double)c.st.width_in[i];  // the seed input is implicit
     c.st.bytes_model[i] = 4.0 * win * (double)c.st.rows_in[i] + 8.0 * (double)c.st.rows_in[i] +
