@@ -252,19 +252,23 @@ def main():
     value = total_count / (max_ms / 1000.0)
 
     # ---------------- roofline of the dominant kernel (SURVEY §8(d) byte model)
-    kinds = {"k_step<count>": [0.0, 0.0, 0], "k_step<write>": [0.0, 0.0, 0]}
+    # Launch kinds: "single" = the fused join step of every materialized level (single pass:
+    # join + filters + look-back prefix + write), "count" = the count-only last step.  Bytes per
+    # launch follow SURVEY §8(d): read rows 4*w*|F_i| (0 for the implicit seed) + key lookups
+    # 8*|F_i| + candidates 4*C_i + probes 4*Q_i (+ write 4*w_{i+1}*|F_{i+1}| for "single").
+    kinds = {"join_single": [0.0, 0.0, 0], "join_count": [0.0, 0.0, 0]}
     for s in stats:
         for i in range(s["num_steps"]):
             win = 0 if i == 0 else s["width_in"][i]
             read = 4.0 * win * s["rows_in"][i] + 8.0 * s["rows_in"][i] + 4.0 * s["candidates"][i] + 4.0 * s["probes"][i]
-            last_count = (i == s["num_steps"] - 1)
-            kinds["k_step<count>"][0] += s["ms_count"][i]
-            kinds["k_step<count>"][1] += read
-            kinds["k_step<count>"][2] += 1
-            if not last_count:
-                kinds["k_step<write>"][0] += s["ms_write"][i]
-                kinds["k_step<write>"][1] += read + 4.0 * s["width_out"][i] * s["rows_out"][i]
-                kinds["k_step<write>"][2] += 1
+            if s["ms_count"][i] > 0:
+                kinds["join_count"][0] += s["ms_count"][i]
+                kinds["join_count"][1] += read
+                kinds["join_count"][2] += 1
+            if s["ms_write"][i] > 0:
+                kinds["join_single"][0] += s["ms_write"][i]
+                kinds["join_single"][1] += read + 4.0 * s["width_out"][i] * s["rows_out"][i]
+                kinds["join_single"][2] += 1
     dom = max(kinds, key=lambda kk: kinds[kk][0])
     ms, byts, launches = kinds[dom]
     peak, peak_src = load_peaks()
@@ -277,12 +281,16 @@ def main():
         except Exception:
             traffic = None
     total_model = sum(sum(s["bytes_model"]) for s in stats)
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": achieved / peak, "traffic": traffic,
-            "bytes_per_launch": byts / max(1, launches), "ms_per_launch": ms / max(1, launches),
+    roof = {"bound": "hbm", "kernel": dom + " (k_rows/k_step, extend.cu)", "achieved": achieved,
+            "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic["bytes_per_launch"] if isinstance(traffic, dict) else traffic,
+            "algorithmic_bytes_per_launch": byts / max(1, launches),
+            "ms_per_launch": ms / max(1, launches), "launches": launches,
             "peak_source": peak_src, "kernel_share_of_step": ms / max(1e-9, sum(times)),
             "step_model_GBps": (total_model / 1e9) / (sum(times) / 1e3),
             "bytes_model_per_embedding": total_model / max(1.0, float(count))}
+    if isinstance(traffic, dict):
+        roof["traffic_source"] = traffic.get("source")
 
     # ---------------- end to end through the public API from pinned host buffers
     e2e_val = None
