@@ -86,6 +86,20 @@ __device__ __forceinline__ bool in_row(const int32_t *row, int ws, int32_t x) {
   return hit;
 }
 
+// compile-time width variant (NQ = ws/4 chunks, fully unrolled; NQ == 0 -> runtime loop)
+template <int NQ>
+__device__ __forceinline__ bool in_row_q(const int32_t *row, int ws, int32_t x) {
+  if (NQ == 0) return in_row(row, ws, x);
+  const int4 *r4 = reinterpret_cast<const int4 *>(row);
+  bool hit = false;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int4 v = r4[q];
+    hit |= (v.x == x) | (v.y == x) | (v.z == x) | (v.w == x);
+  }
+  return hit;
+}
+
 // shared-memory row stride (words): the global stride padded to an odd number of int4 chunks
 __host__ __device__ inline int smem_stride(int w) {
   const int ws = row_stride(w);
@@ -198,12 +212,14 @@ __device__ __forceinline__ int32_t colval(const int32_t *row, int w, int c, int3
 
 // Filters for new vertex j with candidate value x (anchor column `acol` is satisfied by
 // construction): all-distinct, closing-edge probes, induced non-edge probes.
+template <int NQ = 0>
 __device__ __forceinline__ bool accept(const DevStep &st, int j, const int32_t *row, int w, int ws,
                                        int32_t x0, int32_t x, int acol,
                                        const int64_t *__restrict__ off,
                                        const int32_t *__restrict__ adj, uint32_t &probes) {
-  if (in_row(row, ws, x)) return false;
+  if (in_row_q<NQ>(row, ws, x)) return false;
   if (j == 1 && x == x0) return false;
+  if (st.n_nbr[j] <= 1 && st.n_non[j] == 0) return true;  // the anchor is the only key
   for (int t = 0; t < st.n_nbr[j]; ++t) {
     int c = st.nbr[j][t];
     if (c == acol) continue;
@@ -582,7 +598,7 @@ __global__ void __launch_bounds__(kStepThreads)
 // per-round scans and barriers.  Survivors go to per-thread slots (kRowSlots each); a thread
 // that overflows its slots marks the tile unwritten and the host re-runs it with the general
 // kernel (kModeWrite).  Output order is identical to k_step (row, then candidate order).
-template <int MODE>
+template <int MODE, int NQ>
 __global__ void __launch_bounds__(kStepThreads)
     k_rows(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
@@ -627,7 +643,7 @@ __global__ void __launch_bounds__(kStepThreads)
     for (int64_t e = e0; e < e0 + ad; ++e) {
       const int32_t x0 = __ldg(adj + e);
       ++my_cand;
-      if (!accept(st, 0, row, w, ws, 0, x0, ac, off, adj, my_probe)) continue;
+      if (!accept<NQ>(st, 0, row, w, ws, 0, x0, ac, off, adj, my_probe)) continue;
       if (st.n_new == 1) {
         if (kStage) {
           if (ns < S) sv_x[2 * (tid * S + ns)] = x0;
@@ -643,7 +659,7 @@ __global__ void __launch_bounds__(kStepThreads)
       for (int64_t f = f0; f < f0 + bd; ++f) {
         const int32_t x1 = __ldg(adj + f);
         ++my_cand;
-        if (!accept(st, 1, row, w, ws, x0, x1, bc, off, adj, my_probe)) continue;
+        if (!accept<NQ>(st, 1, row, w, ws, x0, x1, bc, off, adj, my_probe)) continue;
         if (kStage) {
           if (ns < S) {
             const int sl = tid * S + ns;
@@ -716,7 +732,7 @@ __global__ void k_status_to_excl(const unsigned long long *__restrict__ status, 
 // Raise the dynamic shared-memory limit of a kernel once per (device, kernel) growth.
 cudaError_t prep(const void *fn, int which, size_t smem) {
   static std::mutex mu;
-  static size_t configured[64][6] = {};
+  static size_t configured[64][48] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -725,6 +741,36 @@ cudaError_t prep(const void *fn, int which, size_t smem) {
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess && dev < 64) configured[dev][which] = smem;
   return e;
+}
+
+template <int MODE, int NQ>
+cudaError_t launch_rows_nq(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
+                           size_t smem, cudaStream_t s) {
+  cudaError_t e = prep((const void *)k_rows<MODE, NQ>, 3 * (NQ + 1) + MODE, smem);
+  if (e != cudaSuccess) return e;
+  k_rows<MODE, NQ><<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
+  return cudaGetLastError();
+}
+
+// row-serial kernel specialised on the row width (16-byte chunks per row)
+template <int MODE>
+cudaError_t launch_rows(int nq, const DevStep &st, const StepIO &io, const dm_graph &g,
+                        int64_t tiles, size_t smem, cudaStream_t s) {
+  switch (nq) {
+    case 1: return launch_rows_nq<MODE, 1>(st, io, g, tiles, smem, s);
+    case 2: return launch_rows_nq<MODE, 2>(st, io, g, tiles, smem, s);
+    case 3: return launch_rows_nq<MODE, 3>(st, io, g, tiles, smem, s);
+    case 4: return launch_rows_nq<MODE, 4>(st, io, g, tiles, smem, s);
+    case 5: return launch_rows_nq<MODE, 5>(st, io, g, tiles, smem, s);
+    case 6: return launch_rows_nq<MODE, 6>(st, io, g, tiles, smem, s);
+    case 7: return launch_rows_nq<MODE, 7>(st, io, g, tiles, smem, s);
+    case 8: return launch_rows_nq<MODE, 8>(st, io, g, tiles, smem, s);
+    case 9: return launch_rows_nq<MODE, 9>(st, io, g, tiles, smem, s);
+    case 10: return launch_rows_nq<MODE, 10>(st, io, g, tiles, smem, s);
+    case 11: return launch_rows_nq<MODE, 11>(st, io, g, tiles, smem, s);
+    case 12: return launch_rows_nq<MODE, 12>(st, io, g, tiles, smem, s);
+    default: return launch_rows_nq<MODE, 0>(st, io, g, tiles, smem, s);
+  }
 }
 
 // Low-degree graphs take the row-serial kernel (count and single-pass launches); re-runs at
@@ -741,10 +787,7 @@ cudaError_t launch(const DevStep &st, const StepIO &io, const dm_graph &g, int64
     StepIO io2 = io;
     io2.slots = row_slots(st, g);
     size_t smem = rows_smem_bytes(st.in_w, MODE != kModeCount, io2.slots);
-    cudaError_t e = prep((const void *)k_rows<MODE>, 3 + MODE, smem);
-    if (e != cudaSuccess) return e;
-    k_rows<MODE><<<(unsigned)num_tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);
-    return cudaGetLastError();
+    return launch_rows<MODE>(row_stride(st.in_w) >> 2, st, io2, g, num_tiles, smem, s);
   }
   size_t smem = smem_bytes(st.in_w, MODE != kModeCount);
   cudaError_t e = prep((const void *)k_step<MODE>, MODE, smem);
