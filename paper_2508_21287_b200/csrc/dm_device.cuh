@@ -16,6 +16,7 @@ struct dm_graph {
   int32_t max_deg = 0;
   int64_t *d_off = nullptr;  // [n+1]
   int32_t *d_adj = nullptr;  // [arcs], each list sorted ascending
+  int32_t *d_ell = nullptr;  // max degree <= 4: [n][4] adjacency (ELL, sorted, -1 padded)
 };
 
 namespace dm {
@@ -82,6 +83,7 @@ struct StepIO {
                               //   (init = #tiles), [2] += survivors
   uint64_t cap;               // single pass: output capacity in rows
   int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
+  const int32_t *ell;         // row-serial kernel: ELL adjacency (max degree <= 4) or nullptr
 };
 
 size_t step_smem_bytes(int in_w, bool write_pass);

@@ -253,6 +253,59 @@ __device__ __forceinline__ int pick_anchor(const DevStep &st, int j, const int32
   return best;
 }
 
+// ---- ELL (max degree <= 4) variants: a vertex's whole sorted neighbour list is one int4
+__device__ __forceinline__ int4 ell_row(const int4 *__restrict__ ell, int32_t v) { return __ldg(ell + v); }
+__device__ __forceinline__ int ell_deg(const int4 &e) {
+  return (e.x >= 0) + (e.y >= 0) + (e.z >= 0) + (e.w >= 0);
+}
+__device__ __forceinline__ int32_t ell_at(const int4 &e, int i) {
+  return i == 0 ? e.x : (i == 1 ? e.y : (i == 2 ? e.z : e.w));
+}
+__device__ __forceinline__ bool ell_has(const int4 *__restrict__ ell, int32_t u, int32_t x) {
+  const int4 e = ell_row(ell, u);
+  return (e.x == x) | (e.y == x) | (e.z == x) | (e.w == x);
+}
+
+// key column with the smallest-degree image for new vertex j; returns its ELL row in `nb`
+__device__ __forceinline__ int pick_anchor_ell(const DevStep &st, int j, const int32_t *row, int w,
+                                               int32_t x0, const int4 *__restrict__ ell, int4 &nb) {
+  int best = st.nbr[j][0];
+  nb = ell_row(ell, colval(row, w, best, x0));
+  if (st.n_nbr[j] == 1) return best;
+  int bd = ell_deg(nb);
+  for (int t = 1; t < st.n_nbr[j]; ++t) {
+    const int c = st.nbr[j][t];
+    const int4 e = ell_row(ell, colval(row, w, c, x0));
+    const int d = ell_deg(e);
+    if (d < bd) {
+      bd = d;
+      nb = e;
+      best = c;
+    }
+  }
+  return best;
+}
+
+template <int NQ>
+__device__ __forceinline__ bool accept_ell(const DevStep &st, int j, const int32_t *row, int w,
+                                           int ws, int32_t x0, int32_t x, int acol,
+                                           const int4 *__restrict__ ell, uint32_t &probes) {
+  if (in_row_q<NQ>(row, ws, x)) return false;
+  if (j == 1 && x == x0) return false;
+  if (st.n_nbr[j] <= 1 && st.n_non[j] == 0) return true;
+  for (int t = 0; t < st.n_nbr[j]; ++t) {
+    const int c = st.nbr[j][t];
+    if (c == acol) continue;
+    ++probes;
+    if (!ell_has(ell, colval(row, w, c, x0), x)) return false;
+  }
+  for (int t = 0; t < st.n_non[j]; ++t) {
+    ++probes;
+    if (ell_has(ell, colval(row, w, st.non[j][t], x0), x)) return false;
+  }
+  return true;
+}
+
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 struct SmemLayout {
@@ -598,7 +651,7 @@ __global__ void __launch_bounds__(kStepThreads)
 // per-round scans and barriers.  Survivors go to per-thread slots (kRowSlots each); a thread
 // that overflows its slots marks the tile unwritten and the host re-runs it with the general
 // kernel (kModeWrite).  Output order is identical to k_step (row, then candidate order).
-template <int MODE, int NQ>
+template <int MODE, int NQ, bool ELL>
 __global__ void __launch_bounds__(kStepThreads)
     k_rows(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
@@ -634,7 +687,45 @@ __global__ void __launch_bounds__(kStepThreads)
   int ns = 0;
   bool ovf = false;
   uint32_t my_cand = 0, my_probe = 0;
-  if (tid < nrows) {
+  auto record = [&](int32_t x0, int32_t x1) {
+    if (kStage) {
+      if (ns < S) {
+        const int sl = tid * S + ns;
+        sv_x[2 * sl] = x0;
+        sv_x[2 * sl + 1] = x1;
+      } else {
+        ovf = true;
+      }
+    }
+    ++ns;
+  };
+  if (tid < nrows && ELL) {
+    // max degree <= 4: candidate lists are single int4 loads (sorted, -1 padded)
+    const int32_t *row = rows + tid * ss;
+    const int4 *ell = reinterpret_cast<const int4 *>(io.ell);
+    int4 na;
+    const int ac = pick_anchor_ell(st, 0, row, w, 0, ell, na);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int32_t x0 = ell_at(na, i);
+      if (x0 < 0) break;
+      ++my_cand;
+      if (!accept_ell<NQ>(st, 0, row, w, ws, 0, x0, ac, ell, my_probe)) continue;
+      if (st.n_new == 1) {
+        record(x0, -1);
+        continue;
+      }
+      int4 nb;
+      const int bc = pick_anchor_ell(st, 1, row, w, x0, ell, nb);
+#pragma unroll
+      for (int i1 = 0; i1 < 4; ++i1) {
+        const int32_t x1 = ell_at(nb, i1);
+        if (x1 < 0) break;
+        ++my_cand;
+        if (accept_ell<NQ>(st, 1, row, w, ws, x0, x1, bc, ell, my_probe)) record(x0, x1);
+      }
+    }
+  } else if (tid < nrows) {
     const int32_t *row = rows + tid * ss;
     int32_t av;
     int64_t ad;
@@ -645,11 +736,7 @@ __global__ void __launch_bounds__(kStepThreads)
       ++my_cand;
       if (!accept<NQ>(st, 0, row, w, ws, 0, x0, ac, off, adj, my_probe)) continue;
       if (st.n_new == 1) {
-        if (kStage) {
-          if (ns < S) sv_x[2 * (tid * S + ns)] = x0;
-          else ovf = true;
-        }
-        ++ns;
+        record(x0, -1);
         continue;
       }
       int32_t bv;
@@ -659,17 +746,7 @@ __global__ void __launch_bounds__(kStepThreads)
       for (int64_t f = f0; f < f0 + bd; ++f) {
         const int32_t x1 = __ldg(adj + f);
         ++my_cand;
-        if (!accept<NQ>(st, 1, row, w, ws, x0, x1, bc, off, adj, my_probe)) continue;
-        if (kStage) {
-          if (ns < S) {
-            const int sl = tid * S + ns;
-            sv_x[2 * sl] = x0;
-            sv_x[2 * sl + 1] = x1;
-          } else {
-            ovf = true;
-          }
-        }
-        ++ns;
+        if (accept<NQ>(st, 1, row, w, ws, x0, x1, bc, off, adj, my_probe)) record(x0, x1);
       }
     }
   }
@@ -732,7 +809,7 @@ __global__ void k_status_to_excl(const unsigned long long *__restrict__ status, 
 // Raise the dynamic shared-memory limit of a kernel once per (device, kernel) growth.
 cudaError_t prep(const void *fn, int which, size_t smem) {
   static std::mutex mu;
-  static size_t configured[64][48] = {};
+  static size_t configured[64][96] = {};
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
@@ -746,9 +823,17 @@ cudaError_t prep(const void *fn, int which, size_t smem) {
 template <int MODE, int NQ>
 cudaError_t launch_rows_nq(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
                            size_t smem, cudaStream_t s) {
-  cudaError_t e = prep((const void *)k_rows<MODE, NQ>, 3 * (NQ + 1) + MODE, smem);
+  if (g.d_ell) {
+    StepIO io2 = io;
+    io2.ell = g.d_ell;
+    cudaError_t e = prep((const void *)k_rows<MODE, NQ, true>, 48 + 3 * (NQ + 1) + MODE, smem);
+    if (e != cudaSuccess) return e;
+    k_rows<MODE, NQ, true><<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);
+    return cudaGetLastError();
+  }
+  cudaError_t e = prep((const void *)k_rows<MODE, NQ, false>, 3 * (NQ + 1) + MODE, smem);
   if (e != cudaSuccess) return e;
-  k_rows<MODE, NQ><<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
+  k_rows<MODE, NQ, false><<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io, g.d_off, g.d_adj);
   return cudaGetLastError();
 }
 
@@ -765,10 +850,6 @@ cudaError_t launch_rows(int nq, const DevStep &st, const StepIO &io, const dm_gr
     case 6: return launch_rows_nq<MODE, 6>(st, io, g, tiles, smem, s);
     case 7: return launch_rows_nq<MODE, 7>(st, io, g, tiles, smem, s);
     case 8: return launch_rows_nq<MODE, 8>(st, io, g, tiles, smem, s);
-    case 9: return launch_rows_nq<MODE, 9>(st, io, g, tiles, smem, s);
-    case 10: return launch_rows_nq<MODE, 10>(st, io, g, tiles, smem, s);
-    case 11: return launch_rows_nq<MODE, 11>(st, io, g, tiles, smem, s);
-    case 12: return launch_rows_nq<MODE, 12>(st, io, g, tiles, smem, s);
     default: return launch_rows_nq<MODE, 0>(st, io, g, tiles, smem, s);
   }
 }

@@ -58,6 +58,21 @@ __global__ void k_max_degree(const int64_t *__restrict__ off, int32_t n, int *__
   if (threadIdx.x == 0) atomicMax(out, r);
 }
 
+// ELL copy of a max-degree-4 adjacency: one 16-byte load returns a vertex's whole sorted list
+__global__ void k_build_ell(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                            int32_t n, int4 *__restrict__ ell) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = off[v], d = off[v + 1] - b;
+    int4 e;
+    e.x = d > 0 ? adj[b] : -1;
+    e.y = d > 1 ? adj[b + 1] : -1;
+    e.z = d > 2 ? adj[b + 2] : -1;
+    e.w = d > 3 ? adj[b + 3] : -1;
+    ell[v] = e;
+  }
+}
+
 int grid_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
@@ -106,6 +121,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
     cleanup();
     cudaFree(g->d_off);
     cudaFree(g->d_adj);
+    cudaFree(g->d_ell);
     delete g;
     return st;
   };
@@ -172,6 +188,12 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   }
   GC(cudaStreamSynchronize(s));
   g->max_deg = hmax;
+  if (n > 0 && hmax <= 4) {
+    GC(cudaMalloc(&g->d_ell, sizeof(int4) * (size_t)n));
+    k_build_ell<<<grid_for(n), 256, 0, s>>>(g->d_off, g->d_adj, n, reinterpret_cast<int4 *>(g->d_ell));
+    GC(cudaGetLastError());
+    GC(cudaStreamSynchronize(s));
+  }
 #undef GC
   cleanup();
   *out = g;
@@ -193,6 +215,7 @@ void dm_graph_destroy(dm_graph *g) {
   dm::DeviceGuard dg(g->device);
   cudaFree(g->d_off);
   cudaFree(g->d_adj);
+  cudaFree(g->d_ell);
   delete g;
 }
 
