@@ -49,6 +49,12 @@ WORKLOADS = {
                    lambda: gen.rmat(20, 16, seed=1), gen.diamond, True),
     "c4-k4": ("config4: 4-clique into R-MAT scale 20 edge factor 16, count",
               lambda: gen.rmat(20, 16, seed=1), lambda: gen.clique(4), True),
+    "c4-diamond-s16": ("config4 (down-scaled): diamond into R-MAT scale 16, count",
+                       lambda: gen.rmat(16, 16, seed=1), gen.diamond, True),
+    "c4-k4-s16": ("config4 (down-scaled): 4-clique into R-MAT scale 16, count",
+                  lambda: gen.rmat(16, 16, seed=1), lambda: gen.clique(4), True),
+    "c4-diamond-s18": ("config4 (down-scaled): diamond into R-MAT scale 18, count",
+                       lambda: gen.rmat(18, 16, seed=1), gen.diamond, True),
     "c3-p20": ("config3: P20 into IBM heavy-hex w=10 (1121 V), count",
                lambda: gen.ibm_heavy_hex(10), lambda: gen.path(20), False),
     "c2-er-c4": ("config2: C4 into ER G(1e4, 8e4) seed 1, count",

@@ -77,7 +77,7 @@ EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_
            "dm_graph_num_vertices", "dm_graph_num_arcs", "dm_graph_max_degree",
            "dm_graph_device", "dm_graph_device_csr", "dm_graph_copy_csr", "dm_match",
            "dm_result_count", "dm_result_width", "dm_result_rows", "dm_result_stats",
-           "dm_result_free", "dm_last_error", "dm_plan_create", "dm_plan_destroy",
+           "dm_result_free", "dm_last_error", "dm_plan_create", "dm_plan_create_ex", "dm_plan_destroy",
            "dm_plan_num_slices", "dm_plan_slice", "dm_plan_num_steps", "dm_plan_first_vertex",
            "dm_plan_describe"]
 
@@ -112,6 +112,8 @@ def lib():
         "dm_result_free": (None, [P]),
         "dm_last_error": (c.c_char_p, []),
         "dm_plan_create": (c.c_int, [c.c_int32, P, c.c_int64, c.c_int32, c.c_int32, c.POINTER(P)]),
+        "dm_plan_create_ex": (c.c_int, [c.c_int32, P, c.c_int64, c.c_int32, c.c_int32, c.c_double,
+                                        c.c_double, c.c_double, c.c_double, c.c_int32, c.POINTER(P)]),
         "dm_plan_destroy": (None, [P]),
         "dm_plan_num_slices": (c.c_int32, [P]),
         "dm_plan_slice": (c.c_int, [P, c.c_int32, c.POINTER(c.c_int32), c.POINTER(c.c_int32),
@@ -151,12 +153,21 @@ def _motifs(m) -> int:
 class Plan:
     """Host join program (dm_plan_create): the §3.3 decomposition and the executed steps."""
 
-    def __init__(self, k: int, p_edges, motifs="all", mode: str = "mono"):
+    def __init__(self, k: int, p_edges, motifs="all", mode: str = "mono", stats=None):
+        """stats: optional dict(n, arcs, sum_d2, closure, count_only) for the join-order cost
+        model (dm_plan_create_ex); default = dm_plan_create's sparse-lattice defaults."""
         L = lib()
         pe = _edges_arr(p_edges)
         h = ctypes.c_void_p()
-        _check(L.dm_plan_create(k, pe.ctypes.data if pe.size else None, pe.shape[0], _motifs(motifs),
-                                DM_INDUCED if mode == "induced" else DM_MONO, ctypes.byref(h)))
+        md = DM_INDUCED if mode == "induced" else DM_MONO
+        if stats is None:
+            _check(L.dm_plan_create(k, pe.ctypes.data if pe.size else None, pe.shape[0],
+                                    _motifs(motifs), md, ctypes.byref(h)))
+        else:
+            _check(L.dm_plan_create_ex(k, pe.ctypes.data if pe.size else None, pe.shape[0],
+                                       _motifs(motifs), md, float(stats["n"]), float(stats["arcs"]),
+                                       float(stats["sum_d2"]), float(stats.get("closure", 0.0)),
+                                       int(bool(stats.get("count_only", False))), ctypes.byref(h)))
         self._h = h
 
     def __del__(self):

@@ -17,6 +17,8 @@ struct dm_graph {
   int64_t *d_off = nullptr;  // [n+1]
   int32_t *d_adj = nullptr;  // [arcs], each list sorted ascending
   int32_t *d_ell = nullptr;  // max degree <= 4: [n][4] adjacency (ELL, sorted, -1 padded)
+  double sum_d2 = 0.0;       // sum of squared degrees (size-biased degree = sum_d2 / arcs)
+  double closure = 0.0;      // sampled P[c in N(a) | a-b-c wedge] (triangle closure)
 };
 
 namespace dm {
@@ -48,6 +50,8 @@ constexpr int kSurvBuf = 1024;      // survivors staged in shared memory per CTA
 constexpr int kRowSlotsMax = 8;     // row-serial kernel: max survivor slots per frontier row
 constexpr int kRowSerialDeg1 = 16;  // row-serial kernel for 1-vertex steps if max degree <= 16
 constexpr int kRowSerialDeg2 = 4;   //   ... and for 2-vertex steps if max degree <= 4
+constexpr int kPairSmem = 1024;     // shared-key pair kernel: per-warp list in shared memory
+constexpr int kPairBatch = 16;      //   rows claimed per atomic
 constexpr int kAccSlots = 64;       // counters are spread over 64 slots (atomic contention)
 constexpr int kModeCount = 0;       // join-step kernel launch modes (see extend.cu)
 constexpr int kModeWrite = 1;
@@ -93,6 +97,10 @@ cudaError_t launch_step_write(const DevStep &st, const StepIO &io, const dm_grap
                               int64_t num_tiles, cudaStream_t s);
 cudaError_t launch_step_single(const DevStep &st, const StepIO &io, const dm_graph &g,
                                int64_t num_tiles, cudaStream_t s);
+int pair_mode_of(const DevStep &st);
+bool row_serial_step(const DevStep &st, const dm_graph &g);
+cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g, int pair_mode,
+                         cudaStream_t s);
 cudaError_t launch_status_to_excl(const unsigned long long *status, int64_t tiles, uint64_t *excl,
                                   cudaStream_t s);
 

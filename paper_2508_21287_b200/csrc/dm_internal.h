@@ -49,7 +49,10 @@ struct Step {
 // Data-graph statistics for the join-order cost model (defaults: a sparse lattice).
 struct PlanStats {
   double n = 10000.0;
-  double avg_degree = 3.0;
+  double avg_degree = 3.0;   // arcs / n: expansion from the implicit vertex table
+  double fwd_degree = 3.0;   // sum d^2 / arcs: degree of a vertex reached along an edge
+  double closure = 0.0;      // P[extra join key holds] beyond the random-pair probability
+  bool count_only = false;   // last level is counted, not materialized
 };
 
 struct Plan {

@@ -73,6 +73,48 @@ __global__ void k_build_ell(const int64_t *__restrict__ off, const int32_t *__re
   }
 }
 
+// sum of squared degrees (double, one atomic per block)
+__global__ void k_sum_d2(const int64_t *__restrict__ off, int32_t n, double *__restrict__ out) {
+  double acc = 0.0;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const double d = (double)(off[v + 1] - off[v]);
+    acc += d * d;
+  }
+  typedef cub::BlockReduce<double, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const double r = BR(tmp).Sum(acc);
+  if (threadIdx.x == 0) atomicAdd(out, r);
+}
+
+// Triangle closure on a deterministic sample of arcs (a,b): sum over samples of
+// |N(a) & N(b)| and of (deg(b) - 1) (wedges a-b-c); ratio = closure probability.
+__global__ void k_sample_closure(const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
+                                 int32_t n, int64_t arcs, int samples, double *__restrict__ out) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < samples; s += gridDim.x * blockDim.x) {
+    const uint64_t h = (uint64_t)(s + 1) * 0x9E3779B97F4A7C15ull;
+    const int64_t e = (int64_t)((h >> 11) % (uint64_t)arcs);
+    int64_t lo = 0, hi = n;  // source vertex a of arc e: largest a with off[a] <= e
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (off[mid] <= e) lo = mid;
+      else hi = mid;
+    }
+    const int32_t a = (int32_t)lo, b = adj[e];
+    int64_t i = off[a], ie = off[a + 1], j = off[b], je = off[b + 1];
+    const double wedges = (double)(je - j - 1);
+    double t = 0.0;
+    while (i < ie && j < je) {  // merge intersection of two sorted lists
+      const int32_t x = adj[i], y = adj[j];
+      t += (x == y);
+      i += (x <= y);
+      j += (y <= x);
+    }
+    atomicAdd(out, t);
+    atomicAdd(out + 1, wedges);
+  }
+}
+
 int grid_for(int64_t work) {
   int64_t b = (work + 255) / 256;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
@@ -188,6 +230,24 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   }
   GC(cudaStreamSynchronize(s));
   g->max_deg = hmax;
+  if (n > 0 && arcs > 0) {  // statistics for the join-order cost model
+    double *d_stat = nullptr;
+    GC(cudaMalloc(&d_stat, 3 * sizeof(double)));
+    GC(cudaMemsetAsync(d_stat, 0, 3 * sizeof(double), s));
+    k_sum_d2<<<grid_for(n), 256, 0, s>>>(g->d_off, n, d_stat);
+    const int samples = 4096;
+    k_sample_closure<<<16, 256, 0, s>>>(g->d_off, g->d_adj, n, arcs, samples, d_stat + 1);
+    double hs[3] = {0, 0, 0};
+    cudaError_t e1 = cudaGetLastError();
+    cudaError_t e2 = cudaMemcpyAsync(hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s);
+    cudaError_t e3 = cudaStreamSynchronize(s);
+    cudaFree(d_stat);
+    GC(e1);
+    GC(e2);
+    GC(e3);
+    g->sum_d2 = hs[0];
+    g->closure = hs[2] > 0 ? hs[1] / hs[2] : 0.0;
+  }
   if (n > 0 && hmax <= 4) {
     GC(cudaMalloc(&g->d_ell, sizeof(int4) * (size_t)n));
     k_build_ell<<<grid_for(n), 256, 0, s>>>(g->d_off, g->d_adj, n, reinterpret_cast<int4 *>(g->d_ell));

@@ -222,7 +222,11 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     io.total = c.d_acc;
     Prof::Ev e;
     c.prof.begin(si, 0, e);
-    CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
+    const int pm = pair_mode_of(D);
+    if (pm >= 0 && !row_serial_step(D, *c.g))
+      CK(launch_pairs(D, io, *c.g, pm, c.s), "pair kernel");
+    else
+      CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
     c.prof.end(e);
     c.st.num_launches++;
     return DM_OK;
@@ -424,6 +428,9 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   PlanStats pstats;
   pstats.n = (double)std::max<int32_t>(g->n, 2);
   pstats.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
+  pstats.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
+  pstats.closure = g->closure;
+  pstats.count_only = !(opt.output & DM_OUT_TABLE);
   dm_status stt = build_plan(k, p_edges, pm, opt.motifs, opt.mode, plan, pstats);
   if (stt != DM_OK) return stt;
   int64_t sb = std::max<int64_t>(0, opt.seed_begin);

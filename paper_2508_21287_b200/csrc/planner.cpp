@@ -91,74 +91,122 @@ bool first_match(const Pat &P, const MotifT &M, const std::vector<char> &alive,
 }
 
 
-// Compile a slice execution order into kernel steps.  Each slice contributes its unplaced
-// vertices as one step (ordered so each has a placed pattern neighbour); every pattern edge
-// between a new vertex and a placed vertex is enforced when the later endpoint is placed.
-dm_status compile_order(const Pat &P, int mode, const std::vector<int> &order, int first,
-                        Plan &plan) {
+// Placement order of a slice execution order: the first vertex, then each slice's unplaced
+// vertices (each with a placed pattern neighbour -- slices are connected).
+bool placement_order(const Pat &P, const Plan &plan, const std::vector<int> &order, int first,
+                     std::vector<int> &out) {
   const int k = P.k;
-  plan.steps.clear();
-  plan.col_pvert.clear();
-  plan.pvert_col.assign(k, -1);
-  plan.order = order;
-  auto place = [&](int pv) {
-    plan.pvert_col[pv] = (int)plan.col_pvert.size();
-    plan.col_pvert.push_back(pv);
-  };
-  plan.first_vertex = first;
-  place(first);
+  std::vector<char> placed(k, 0);
+  out.assign(1, first);
+  placed[first] = 1;
   for (int si : order) {
     const Slice &s = plan.slices[(size_t)si];
     std::vector<int> fresh;
     for (int i = 0; i < s.nv; ++i)
-      if (plan.pvert_col[s.v[i]] < 0) fresh.push_back(s.v[i]);
-    if (fresh.empty()) continue;  // pure closing-edge slice: enforced by pushdown
-    Step st;
-    st.slice = si;
-    st.in_w = (int)plan.col_pvert.size();
+      if (!placed[s.v[i]]) fresh.push_back(s.v[i]);
     while (!fresh.empty()) {
       size_t pick = fresh.size();
       for (size_t j = 0; j < fresh.size() && pick == fresh.size(); ++j)
         for (int u = 0; u < k; ++u)
-          if (P.adj[fresh[j]][u] && plan.pvert_col[u] >= 0) { pick = j; break; }
-      if (pick == fresh.size()) return DM_ERR_ARG;
-      const int v = fresh[pick];
+          if (P.adj[fresh[j]][u] && placed[u]) { pick = j; break; }
+      if (pick == fresh.size()) return false;
+      placed[fresh[pick]] = 1;
+      out.push_back(fresh[pick]);
       fresh.erase(fresh.begin() + (long)pick);
-      if (st.n_new == 2) return DM_ERR_ARG;
-      StepVertex sv;
-      sv.pvert = v;
-      for (int c = 0; c < (int)plan.col_pvert.size(); ++c) {
-        const int u = plan.col_pvert[(size_t)c];
-        if (P.adj[v][u]) sv.nbr[sv.n_nbr++] = c;
-        else if (mode == DM_INDUCED) sv.non[sv.n_non++] = c;
-      }
-      st.nv[st.n_new++] = sv;
-      place(v);
     }
-    plan.steps.push_back(st);
   }
-  return (int)plan.col_pvert.size() == k ? DM_OK : DM_ERR_ARG;
+  return (int)out.size() == k;
 }
 
-// Frontier-size model: level sizes grow by d_avg per new vertex and shrink by the edge
-// probability p = d_avg/(n-1) per extra join key; cost = bytes of every materialized level
-// (written + read once) + one byte-equivalent per candidate per compared column.
-double estimate_cost(const Plan &plan, const PlanStats &st) {
-  const double n = std::max(2.0, st.n), d = std::max(1.0, st.avg_degree);
-  const double p = std::min(1.0, d / (n - 1.0));
-  double rows = n, cost = 0.0;
-  for (size_t i = 0; i < plan.steps.size(); ++i) {
-    const Step &s = plan.steps[i];
-    double cand = 0.0;
-    for (int j = 0; j < s.n_new; ++j) {
-      cand += rows * d;
-      rows *= d * std::pow(p, s.nv[j].n_nbr - 1);
+// Frontier-size model for one step placing vertices ord[pos..pos+nv) after `pos` placed
+// vertices: the first expansion from the implicit vertex table grows rows by avg_degree, later
+// ones by the size-biased degree; every extra join key keeps a fraction
+// q = max(closure, d/(n-1)).  A 2-vertex count-only last step whose second vertex has the same
+// keys as the first (a "shared-key pair", e.g. both apexes of a diamond) enumerates pairs of
+// the first vertex's list.  Cost = candidates x compared columns + bytes of every materialized
+// level (written + read).
+struct StepCost {
+  double rows_out, cost;
+};
+StepCost step_cost(const Pat &P, const std::vector<int> &ord, int pos, int nv, double rows,
+                   bool last, const PlanStats &st) {
+  const double n = std::max(2.0, st.n);
+  const double d1 = std::max(1.0, st.avg_degree), d2 = std::max(1.0, st.fwd_degree);
+  const double q = std::min(1.0, std::max(st.closure, d1 / (n - 1.0)));
+  double cost = 0.0, r = rows;
+  int keys0 = 0;
+  for (int j = 0; j < nv; ++j) {
+    const int v = ord[(size_t)(pos + j)];
+    int keys = 0;
+    for (int i = 0; i < pos + j; ++i) keys += P.adj[v][ord[(size_t)i]] ? 1 : 0;
+    const double dexp = (pos == 1 && j == 0) ? d1 : d2;
+    const bool shared = j == 1 && last && st.count_only &&
+                        keys - (P.adj[v][ord[(size_t)pos]] ? 1 : 0) == keys0;
+    if (shared) {
+      const double list = std::max(1.0, r / std::max(1.0, rows));  // first vertex's list per row
+      cost += r * list * (pos + j + 1);
+      r *= list * (P.adj[v][ord[(size_t)pos]] ? q : 1.0);
+    } else {
+      cost += r * dexp * (pos + j + 1);
+      r *= dexp * std::pow(q, keys - 1);
     }
-    cost += cand * (s.in_w + 1);
-    const int wout = s.in_w + s.n_new;
-    if (i + 1 < plan.steps.size()) cost += 2.0 * 4.0 * rows * ((wout + 3) & ~3);
+    keys0 = keys;
   }
-  return cost;
+  if (!last || !st.count_only) cost += 2.0 * 4.0 * r * (double)(((pos + nv) + 3) & ~3);
+  return {r, cost};
+}
+
+// Compile a placement order into kernel steps: consecutive groups of 1 or 2 vertices chosen
+// by dynamic programming over the frontier-size model (the rows after a prefix do not depend
+// on the grouping).  Every pattern edge between a new vertex and an earlier one is enforced
+// when the later endpoint is placed (selection pushdown, DESIGN R1).
+double compile_order(const Pat &P, int mode, const std::vector<int> &ord, Plan &plan,
+                     const PlanStats &st) {
+  const int k = P.k;
+  plan.steps.clear();
+  plan.col_pvert = ord;
+  plan.pvert_col.assign(k, -1);
+  for (int c = 0; c < k; ++c) plan.pvert_col[ord[(size_t)c]] = c;
+  plan.first_vertex = ord[0];
+  std::vector<double> rows(k + 1, 0.0);  // rows after each prefix (grouping independent)
+  rows[1] = std::max(2.0, st.n);
+  for (int i = 1; i < k; ++i) rows[i + 1] = step_cost(P, ord, i, 1, rows[i], false, st).rows_out;
+  const double INF = 1e300;
+  std::vector<double> best(k + 1, INF);
+  std::vector<int> take(k + 1, 0);
+  best[1] = 0.0;
+  for (int i = 2; i <= k; ++i) {
+    for (int g = 1; g <= 2 && g < i; ++g) {
+      const int pos = i - g;
+      if (best[pos] >= INF) continue;
+      const double c = best[pos] + step_cost(P, ord, pos, g, rows[pos], i == k, st).cost;
+      if (c < best[i]) {
+        best[i] = c;
+        take[i] = g;
+      }
+    }
+  }
+  std::vector<int> groups;
+  for (int i = k; i > 1; i -= take[i]) groups.push_back(take[i]);
+  std::reverse(groups.begin(), groups.end());
+  int pos = 1;
+  for (int g : groups) {
+    Step stp;
+    stp.in_w = pos;
+    for (int j = 0; j < g; ++j) {
+      const int v = ord[(size_t)(pos + j)];
+      StepVertex sv;
+      sv.pvert = v;
+      for (int c = 0; c < pos + j; ++c) {
+        if (P.adj[v][ord[(size_t)c]]) sv.nbr[sv.n_nbr++] = c;
+        else if (mode == DM_INDUCED) sv.non[sv.n_non++] = c;
+      }
+      stp.nv[stp.n_new++] = sv;
+    }
+    plan.steps.push_back(stp);
+    pos += g;
+  }
+  return k == 1 ? 0.0 : best[k];
 }
 
 }  // namespace
@@ -273,8 +321,10 @@ dm_status build_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t moti
       }
       if ((int)order.size() != ns) continue;
       Plan cand = plan;
-      if (compile_order(P, mode, order, plan.slices[seed].v[fv], cand) != DM_OK) continue;
-      const double cost = estimate_cost(cand, stats);
+      std::vector<int> ord;
+      if (!placement_order(P, plan, order, plan.slices[seed].v[fv], ord)) continue;
+      cand.order = order;
+      const double cost = compile_order(P, mode, ord, cand, stats);
       if (best_cost < 0 || cost < best_cost - 1e-9 * best_cost) {
         best_cost = cost;
         best = std::move(cand);
@@ -304,7 +354,7 @@ std::string Plan::describe() const {
   o << "],\"steps\":[";
   for (size_t i = 0; i < steps.size(); ++i) {
     const Step &st = steps[i];
-    o << (i ? "," : "") << "{\"slice\":" << st.slice << ",\"in_w\":" << st.in_w << ",\"new\":[";
+    o << (i ? "," : "") << "{\"in_w\":" << st.in_w << ",\"new\":[";
     for (int j = 0; j < st.n_new; ++j) {
       const StepVertex &sv = st.nv[j];
       o << (j ? "," : "") << "{\"pvert\":" << sv.pvert << ",\"nbr_cols\":[";
@@ -336,6 +386,30 @@ dm_status dm_plan_create(int32_t k, const int32_t *p_edges, int64_t pm, int32_t 
   if (st != DM_OK) {
     delete p;
     return st;
+  }
+  *out = p;
+  return DM_OK;
+}
+
+dm_status dm_plan_create_ex(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs,
+                            int32_t mode, double n, double arcs, double sum_d2, double closure,
+                            int32_t count_only, dm_plan **out) {
+  dm::clear_error();
+  if (!out) return dm::fail(DM_ERR_ARG, "out is NULL");
+  if (!(n >= 1) || !(arcs >= 0) || !(sum_d2 >= 0) || !(closure >= 0))
+    return dm::fail(DM_ERR_ARG, "bad graph statistics");
+  dm_plan *p = new (std::nothrow) dm_plan;
+  if (!p) return dm::fail(DM_ERR_OOM, "host allocation failed");
+  dm::PlanStats st;
+  st.n = n;
+  st.avg_degree = arcs / n;
+  st.fwd_degree = arcs > 0 ? sum_d2 / arcs : 1.0;
+  st.closure = closure;
+  st.count_only = count_only != 0;
+  dm_status s = dm::build_plan(k, p_edges, pm, motifs, mode, p->p, st);
+  if (s != DM_OK) {
+    delete p;
+    return s;
   }
   *out = p;
   return DM_OK;

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "rmat or config4 or parity_random" 2>&1 | tail -3
+for wl in c4-k4-s16 c4-diamond-s18; do
+  timeout 300 python scripts/prof_step.py $wl 2 2>&1 | head -4
+done
+timeout 900 python scripts/prof_step.py c4-k4 2 2>&1 | tail -3
