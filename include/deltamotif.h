@@ -169,11 +169,13 @@ DM_API dm_status dm_plan_create(int32_t k, const int32_t *p_edges, int64_t pm, i
                          int32_t mode, dm_plan **out);
 /* Same, with the data-graph statistics the join-order cost model uses (dm_match takes them
  * from the dm_graph): n vertices, arcs (= 2|E|), sum of squared degrees, sampled triangle
- * closure probability (0 for triangle-free graphs), count_only (1: last level is counted, not
- * materialized).  dm_plan_create uses n=1e4, arcs=3e4, sum_d2=9e4, closure=0, count_only=0. */
+ * closure probability (0 for triangle-free graphs), max degree (<= 4 allows a 3-4 vertex
+ * count-only last step), count_only (1: last level is counted, not materialized).
+ * dm_plan_create uses n=1e4, arcs=3e4, sum_d2=9e4, closure=0, max degree 2^30, count_only=0. */
 DM_API dm_status dm_plan_create_ex(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs,
                                    int32_t mode, double n, double arcs, double sum_d2,
-                                   double closure, int32_t count_only, dm_plan **out);
+                                   double closure, int32_t max_degree, int32_t count_only,
+                                   dm_plan **out);
 DM_API void dm_plan_destroy(dm_plan *p);
 DM_API int32_t dm_plan_num_slices(const dm_plan *p);
 /* Slice i: motif id (DM_MOTIF_*), its pattern vertices (slot order, n_vertices <= 3) and the

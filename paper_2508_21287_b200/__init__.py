@@ -113,7 +113,8 @@ def lib():
         "dm_last_error": (c.c_char_p, []),
         "dm_plan_create": (c.c_int, [c.c_int32, P, c.c_int64, c.c_int32, c.c_int32, c.POINTER(P)]),
         "dm_plan_create_ex": (c.c_int, [c.c_int32, P, c.c_int64, c.c_int32, c.c_int32, c.c_double,
-                                        c.c_double, c.c_double, c.c_double, c.c_int32, c.POINTER(P)]),
+                                        c.c_double, c.c_double, c.c_double, c.c_int32, c.c_int32,
+                                        c.POINTER(P)]),
         "dm_plan_destroy": (None, [P]),
         "dm_plan_num_slices": (c.c_int32, [P]),
         "dm_plan_slice": (c.c_int, [P, c.c_int32, c.POINTER(c.c_int32), c.POINTER(c.c_int32),
@@ -154,7 +155,7 @@ class Plan:
     """Host join program (dm_plan_create): the §3.3 decomposition and the executed steps."""
 
     def __init__(self, k: int, p_edges, motifs="all", mode: str = "mono", stats=None):
-        """stats: optional dict(n, arcs, sum_d2, closure, count_only) for the join-order cost
+        """stats: optional dict(n, arcs, sum_d2, closure, max_degree, count_only) for the cost
         model (dm_plan_create_ex); default = dm_plan_create's sparse-lattice defaults."""
         L = lib()
         pe = _edges_arr(p_edges)
@@ -167,6 +168,7 @@ class Plan:
             _check(L.dm_plan_create_ex(k, pe.ctypes.data if pe.size else None, pe.shape[0],
                                        _motifs(motifs), md, float(stats["n"]), float(stats["arcs"]),
                                        float(stats["sum_d2"]), float(stats.get("closure", 0.0)),
+                                       int(stats.get("max_degree", 1 << 30)),
                                        int(bool(stats.get("count_only", False))), ctypes.byref(h)))
         self._h = h
 

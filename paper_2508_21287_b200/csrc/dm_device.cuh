@@ -65,10 +65,10 @@ __host__ __device__ inline int row_stride(int w) { return (w + 3) & ~3; }
 struct DevStep {
   int32_t in_w;
   int32_t n_new;
-  int32_t n_nbr[2];
-  int32_t n_non[2];
-  uint8_t nbr[2][DM_MAX_PATTERN];
-  uint8_t non[2][DM_MAX_PATTERN];
+  int32_t n_nbr[kMaxNew];
+  int32_t n_non[kMaxNew];
+  uint8_t nbr[kMaxNew][DM_MAX_PATTERN];
+  uint8_t non[kMaxNew][DM_MAX_PATTERN];
 };
 
 struct StepIO {

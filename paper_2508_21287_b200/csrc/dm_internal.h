@@ -37,13 +37,14 @@ struct StepVertex {
   int non[DM_MAX_PATTERN];
 };
 
-// One executed join step = one slice's new vertices (1 or 2; the seed slice adds up to 2 to
-// the implicit one-column table of all vertices).
+// One executed join step: 1 or 2 new vertices (up to kMaxNew for a count-only last step on a
+// max-degree-4 graph, where the row-serial kernel enumerates them depth-first).
+constexpr int kMaxNew = 4;
 struct Step {
   int slice = -1;
   int in_w = 0;
   int n_new = 0;
-  StepVertex nv[2];
+  StepVertex nv[kMaxNew];
 };
 
 // Data-graph statistics for the join-order cost model (defaults: a sparse lattice).
@@ -53,6 +54,7 @@ struct PlanStats {
   double fwd_degree = 3.0;   // sum d^2 / arcs: degree of a vertex reached along an edge
   double closure = 0.0;      // P[extra join key holds] beyond the random-pair probability
   bool count_only = false;   // last level is counted, not materialized
+  int max_degree = 1 << 30;  // deep (3-4 vertex) last steps need max degree <= 4
 };
 
 struct Plan {

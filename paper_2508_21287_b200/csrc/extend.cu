@@ -306,6 +306,80 @@ __device__ __forceinline__ bool accept_ell(const DevStep &st, int j, const int32
   return true;
 }
 
+
+// ---- depth-first enumeration of a 3-4 vertex count-only last step (ELL graphs): the larger
+// motif joins of PAPER.md §3.5 executed per row without materializing the levels
+__device__ __forceinline__ int32_t colval4(const int32_t *row, int w, int c, const int32_t (&x)[kMaxNew]) {
+  const int k = c - w;
+  return k < 0 ? row[c] : (k == 0 ? x[0] : (k == 1 ? x[1] : (k == 2 ? x[2] : x[3])));
+}
+
+// 64-bit Bloom filter of a row's vertex set: a candidate whose bit is clear cannot be in the
+// row; only set bits pay for the exact LDS.128 scan
+__device__ __forceinline__ unsigned long long bloom_bit(int32_t v) {
+  return 1ull << (((uint32_t)v * 0x9E3779B1u) >> 26);
+}
+
+template <int J, int NQ>
+__device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *row, int w, int ws,
+                                            unsigned long long bloom, int32_t (&x)[kMaxNew],
+                                            const int4 *__restrict__ ell, uint32_t &cand,
+                                            uint32_t &probes) {
+  if constexpr (J >= kMaxNew) {
+    return 1u;
+  } else {
+    if (J >= st.n_new) return 1u;
+    int best = st.nbr[J][0];
+    int4 nb = ell_row(ell, colval4(row, w, best, x));
+    const bool extra = st.n_nbr[J] > 1 || st.n_non[J] > 0;
+    if (st.n_nbr[J] > 1) {
+      int bd = ell_deg(nb);
+      for (int t = 1; t < st.n_nbr[J]; ++t) {
+        const int c = st.nbr[J][t];
+        const int4 e = ell_row(ell, colval4(row, w, c, x));
+        const int d = ell_deg(e);
+        if (d < bd) {
+          bd = d;
+          nb = e;
+          best = c;
+        }
+      }
+    }
+    unsigned tot = 0;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+      const int32_t y = nb.x;  // candidates in ascending order: shift the int4 down
+      nb.x = nb.y;
+      nb.y = nb.z;
+      nb.z = nb.w;
+      nb.w = -1;
+      if (y < 0) break;
+      ++cand;
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < J; ++t) ok &= x[t] != y;  // distinct from the other new vertices
+      if (!ok) continue;
+      if ((bloom & bloom_bit(y)) && in_row_q<NQ>(row, ws, y)) continue;  // ... and from the row
+      if (extra) {
+        for (int t = 0; t < st.n_nbr[J] && ok; ++t) {
+          const int c = st.nbr[J][t];
+          if (c == best) continue;
+          ++probes;
+          ok = ell_has(ell, colval4(row, w, c, x), y);
+        }
+        for (int t = 0; t < st.n_non[J] && ok; ++t) {
+          ++probes;
+          ok = !ell_has(ell, colval4(row, w, st.non[J][t], x), y);
+        }
+        if (!ok) continue;
+      }
+      x[J] = y;
+      tot += dfs_ell<J + 1, NQ>(st, row, w, ws, bloom, x, ell, cand, probes);
+    }
+    return tot;
+  }
+}
+
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
 struct SmemLayout {
@@ -699,7 +773,16 @@ __global__ void __launch_bounds__(kStepThreads)
     }
     ++ns;
   };
-  if (tid < nrows && ELL) {
+  if (MODE == kModeCount && ELL && st.n_new > 2) {
+    if (tid < nrows) {
+      int32_t x[kMaxNew] = {-1, -1, -1, -1};
+      const int32_t *row = rows + tid * ss;
+      unsigned long long bloom = 0;
+      for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
+      ns = (int)dfs_ell<0, NQ>(st, row, w, ws, bloom, x, reinterpret_cast<const int4 *>(io.ell),
+                               my_cand, my_probe);
+    }
+  } else if (tid < nrows && ELL) {
     // max degree <= 4: candidate lists are single int4 loads (sorted, -1 padded)
     const int32_t *row = rows + tid * ss;
     const int4 *ell = reinterpret_cast<const int4 *>(io.ell);

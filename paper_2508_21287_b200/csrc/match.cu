@@ -431,6 +431,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   pstats.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
   pstats.closure = g->closure;
   pstats.count_only = !(opt.output & DM_OUT_TABLE);
+  pstats.max_degree = g->max_deg;
   dm_status stt = build_plan(k, p_edges, pm, opt.motifs, opt.mode, plan, pstats);
   if (stt != DM_OK) return stt;
   int64_t sb = std::max<int64_t>(0, opt.seed_begin);

@@ -175,8 +175,9 @@ double compile_order(const Pat &P, int mode, const std::vector<int> &ord, Plan &
   std::vector<double> best(k + 1, INF);
   std::vector<int> take(k + 1, 0);
   best[1] = 0.0;
+  const bool deep = st.count_only && st.max_degree <= 4;  // row-serial ELL last step
   for (int i = 2; i <= k; ++i) {
-    for (int g = 1; g <= 2 && g < i; ++g) {
+    for (int g = 1; g <= (deep && i == k ? kMaxNew : 2) && g < i; ++g) {
       const int pos = i - g;
       if (best[pos] >= INF) continue;
       const double c = best[pos] + step_cost(P, ord, pos, g, rows[pos], i == k, st).cost;
@@ -393,7 +394,7 @@ dm_status dm_plan_create(int32_t k, const int32_t *p_edges, int64_t pm, int32_t 
 
 dm_status dm_plan_create_ex(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs,
                             int32_t mode, double n, double arcs, double sum_d2, double closure,
-                            int32_t count_only, dm_plan **out) {
+                            int32_t max_degree, int32_t count_only, dm_plan **out) {
   dm::clear_error();
   if (!out) return dm::fail(DM_ERR_ARG, "out is NULL");
   if (!(n >= 1) || !(arcs >= 0) || !(sum_d2 >= 0) || !(closure >= 0))
@@ -406,6 +407,7 @@ dm_status dm_plan_create_ex(int32_t k, const int32_t *p_edges, int64_t pm, int32
   st.fwd_degree = arcs > 0 ? sum_d2 / arcs : 1.0;
   st.closure = closure;
   st.count_only = count_only != 0;
+  st.max_degree = max_degree;
   dm_status s = dm::build_plan(k, p_edges, pm, motifs, mode, p->p, st);
   if (s != DM_OK) {
     delete p;

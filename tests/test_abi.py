@@ -170,3 +170,22 @@ def test_plan_errors(dm):
     assert ei.value.code == -8
     P = dm.Plan(1, np.zeros((0, 2), np.int32))
     assert P.num_steps == 0 and P.first_vertex == 0
+
+
+def test_plan_cost_model_prefers_shared_key_pairs(dm):
+    """With skewed, clustered graph statistics (R-MAT-like) the planner regroups the diamond /
+    4-clique placement so the count-only last step adds both apexes from one edge (shared-key
+    pair); with lattice statistics a path's last step adds two vertices."""
+    rm = dict(n=1 << 20, arcs=31404412, sum_d2=31404412 * 3000.0, closure=0.03, count_only=True)
+    d = dm.Plan(*g.diamond(), stats=rm).describe()
+    assert [len(s["new"]) for s in d["steps"]] == [1, 2]
+    last = d["steps"][-1]["new"]
+    assert sorted(last[0]["nbr_cols"]) == sorted(last[1]["nbr_cols"]) == [0, 1]
+    d = dm.Plan(*g.clique(4), stats=rm).describe()
+    last = d["steps"][-1]["new"]
+    assert len(last) == 2 and sorted(last[1]["nbr_cols"]) == sorted(last[0]["nbr_cols"] + [2])
+    hh = dict(n=9983, arcs=23808, sum_d2=23808 * 2.5, closure=0.0, count_only=True)
+    d = dm.Plan(*g.path(30), stats=hh).describe()
+    assert len(d["steps"][-1]["new"]) == 2 and len(d["steps"]) == 15
+    with pytest.raises(dm.DMError):
+        dm.Plan(*g.path(3), stats=dict(n=0, arcs=1, sum_d2=1))

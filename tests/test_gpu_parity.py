@@ -89,6 +89,29 @@ def test_parity_random_er(dm, motifs, mode):
         _same(dm, n, e, k, pe, mode=mode, motifs=motifs)
 
 
+@pytest.mark.parametrize("mode", ["mono", "induced"])
+def test_parity_count_mode_random(dm, mode):
+    """Count mode (count-only last step: row-serial, candidate-partitioned or shared-key pair
+    kernel depending on degree and plan) against the oracle's count; denser ER graphs make the
+    planner choose shared-key pair last steps."""
+    rng = np.random.default_rng(77 + (mode == "induced"))
+    for trial in range(40):
+        n = int(rng.integers(20, 120))
+        m = int(n * rng.uniform(2.0, 8.0))
+        n, e = g.er_gnm(n, min(m, n * (n - 1) // 2), int(rng.integers(0, 1 << 30)))
+        k, pe = _pattern(rng, int(rng.integers(3, 7)), float(rng.uniform(0.3, 0.9)))
+        G = dm.Graph(n, e)
+        r = G.match(k, pe, mode=mode)
+        o = oracle.match(n, e, k, pe, induced=(mode == "induced"), table=False)
+        assert r.count == o.count, (trial, k, pe.tolist())
+    for pat in (g.diamond(), g.clique(4), g.path(3), g.star(3)):
+        n, e = g.rmat(11, 16, seed=5)
+        G = dm.Graph(n, e, drop_self_loops=True)
+        for mode2 in ("mono", "induced"):
+            assert G.match(*pat, mode=mode2).count == oracle.match(
+                n, e, *pat, drop_self_loops=True, induced=(mode2 == "induced"), table=False).count
+
+
 @pytest.mark.parametrize("case", spec_examples(), ids=lambda c: c[0])
 def test_parity_spec_examples(dm, case):
     name, data, pat, mode, exp, cite = case
