@@ -245,6 +245,8 @@ def main():
     barrier()
     clocks = clk.stop()
     times = [a.elapsed_time(b) for a, b in ev]
+    if os.environ.get("DM_BENCH_DEBUG"):
+        print("step ms:", [round(t, 2) for t in times], "kernel ms:", [round(sum(s["ms_count"]) + sum(s["ms_write"]), 2) for s in stats], file=sys.stderr)
     local_ms = float(sum(times))
     t = torch.tensor([local_ms, float(count)], dtype=torch.float64, device="cuda")
     if dist_on:

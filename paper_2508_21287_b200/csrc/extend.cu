@@ -253,6 +253,12 @@ __device__ __forceinline__ int pick_anchor(const DevStep &st, int j, const int32
   return best;
 }
 
+// 64-bit Bloom filter of a row's vertex set: a candidate whose bit is clear cannot be in the
+// row; only set bits pay for the exact LDS.128 scan
+__device__ __forceinline__ unsigned long long bloom_bit(int32_t v) {
+  return 1ull << (((uint32_t)v * 0x9E3779B1u) >> 26);
+}
+
 // ---- ELL (max degree <= 4) variants: a vertex's whole sorted neighbour list is one int4
 __device__ __forceinline__ int4 ell_row(const int4 *__restrict__ ell, int32_t v) { return __ldg(ell + v); }
 __device__ __forceinline__ int ell_deg(const int4 &e) {
@@ -288,10 +294,11 @@ __device__ __forceinline__ int pick_anchor_ell(const DevStep &st, int j, const i
 
 template <int NQ>
 __device__ __forceinline__ bool accept_ell(const DevStep &st, int j, const int32_t *row, int w,
-                                           int ws, int32_t x0, int32_t x, int acol,
-                                           const int4 *__restrict__ ell, uint32_t &probes) {
-  if (in_row_q<NQ>(row, ws, x)) return false;
+                                           int ws, unsigned long long bloom, int32_t x0, int32_t x,
+                                           int acol, const int4 *__restrict__ ell,
+                                           uint32_t &probes) {
   if (j == 1 && x == x0) return false;
+  if ((bloom & bloom_bit(x)) && in_row_q<NQ>(row, ws, x)) return false;
   if (st.n_nbr[j] <= 1 && st.n_non[j] == 0) return true;
   for (int t = 0; t < st.n_nbr[j]; ++t) {
     const int c = st.nbr[j][t];
@@ -312,12 +319,6 @@ __device__ __forceinline__ bool accept_ell(const DevStep &st, int j, const int32
 __device__ __forceinline__ int32_t colval4(const int32_t *row, int w, int c, const int32_t (&x)[kMaxNew]) {
   const int k = c - w;
   return k < 0 ? row[c] : (k == 0 ? x[0] : (k == 1 ? x[1] : (k == 2 ? x[2] : x[3])));
-}
-
-// 64-bit Bloom filter of a row's vertex set: a candidate whose bit is clear cannot be in the
-// row; only set bits pay for the exact LDS.128 scan
-__device__ __forceinline__ unsigned long long bloom_bit(int32_t v) {
-  return 1ull << (((uint32_t)v * 0x9E3779B1u) >> 26);
 }
 
 template <int J, int NQ>
@@ -786,6 +787,8 @@ __global__ void __launch_bounds__(kStepThreads)
     // max degree <= 4: candidate lists are single int4 loads (sorted, -1 padded)
     const int32_t *row = rows + tid * ss;
     const int4 *ell = reinterpret_cast<const int4 *>(io.ell);
+    unsigned long long bloom = 0;
+    for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
     int4 na;
     const int ac = pick_anchor_ell(st, 0, row, w, 0, ell, na);
 #pragma unroll
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(kStepThreads)
       const int32_t x0 = ell_at(na, i);
       if (x0 < 0) break;
       ++my_cand;
-      if (!accept_ell<NQ>(st, 0, row, w, ws, 0, x0, ac, ell, my_probe)) continue;
+      if (!accept_ell<NQ>(st, 0, row, w, ws, bloom, 0, x0, ac, ell, my_probe)) continue;
       if (st.n_new == 1) {
         record(x0, -1);
         continue;
@@ -805,7 +808,7 @@ __global__ void __launch_bounds__(kStepThreads)
         const int32_t x1 = ell_at(nb, i1);
         if (x1 < 0) break;
         ++my_cand;
-        if (accept_ell<NQ>(st, 1, row, w, ws, x0, x1, bc, ell, my_probe)) record(x0, x1);
+        if (accept_ell<NQ>(st, 1, row, w, ws, bloom, x0, x1, bc, ell, my_probe)) record(x0, x1);
       }
     }
   } else if (tid < nrows) {

@@ -1,6 +1,6 @@
 """Summarise an ncu --metrics launch list (csv) per kernel kind: time share and DRAM bytes
 per launch; writes profiles/traffic.json[workload][kind] for bench.py's roofline.traffic."""
-import csv, json, os, sys, collections
+import csv, json, os, re, sys, collections
 path, workload = sys.argv[1], sys.argv[2]
 rows = [r for r in csv.reader(open(path)) if r]
 h = next(r for r in rows if "Kernel Name" in r)
@@ -14,7 +14,13 @@ tot_t = 0.0
 for (i, k), m in per.items():
     t = m.get("gpu__time_duration.sum", 0.0)
     tot_t += t
-    kind = "join_single" if ("<2>" in k) else ("join_count" if "<0>" in k else ("join_rerun" if "<1>" in k else "other:" + k.split("(")[0][-40:]))
+    mk = re.search(r"k_(?:rows|step)<(\d)", k)
+    if "k_pairs" in k:
+        kind = "join_count"
+    elif mk:
+        kind = {"0": "join_count", "1": "join_rerun", "2": "join_single"}[mk.group(1)]
+    else:
+        kind = "other:" + k.split("(")[0][-40:]
     kinds[kind][0] += 1
     kinds[kind][1] += t
     kinds[kind][2] += m.get("dram__bytes_read.sum", 0.0) + m.get("dram__bytes_write.sum", 0.0)

@@ -222,6 +222,25 @@ def test_config5_p30_count_full(dm):
     assert r2.count == want and r2.stats["num_chunks"] > r.stats["num_chunks"]
 
 
+@pytest.mark.parametrize("w", [3, 10])
+def test_heavy_hex_count_mode_deep_steps(dm, w):
+    """Count mode on max-degree-3 graphs: the planner ends with a 3-4 vertex depth-first step
+    (ELL row-serial kernel); counts must equal the oracle's, for paths, rings, trees and random
+    subgraphs, in both modes."""
+    n, e = g.ibm_heavy_hex(w)
+    G = dm.Graph(n, e)
+    pats = [g.path(7), g.path(12), g.ring(12), g.path(20) if w == 10 else g.path(9)]
+    for s in (1, 2):
+        pats.append(g.device_subtree(n, e, 12, s))
+        k, pe, _ = g.random_connected_subgraph(n, e, 14, s)
+        pats.append((k, pe))
+    for (k, pe) in pats:
+        for mode in ("mono", "induced"):
+            r = G.match(k, pe, mode=mode)
+            o = oracle.match(n, e, k, pe, induced=(mode == "induced"), table=False)
+            assert r.count == o.count, (k, pe.tolist(), mode)
+
+
 def test_config5_random_subgraphs(dm):
     n, e = g.ibm_heavy_hex(31)
     G = dm.Graph(n, e)
