@@ -200,10 +200,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: DM_BENCH_DEVICE pins every rank to one device (functional multi-rank runs on a
+    # single GPU); DM_DIST_BACKEND=gloo then carries the collectives on CPU tensors
+    if os.environ.get("DM_BENCH_DEVICE") is not None:
+        local = int(os.environ["DM_BENCH_DEVICE"])
+    backend = os.environ.get("DM_DIST_BACKEND", "nccl")
+    coll_dev = "cuda" if backend == "nccl" else "cpu"
     torch.cuda.set_device(local)
     dist_on = world > 1
     if dist_on:
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            tdist.init_process_group(backend)
     desc, gfn, pfn, drop = WORKLOADS[args.workload]
     n, e = gfn()
     k, pe = pfn()
@@ -248,7 +257,7 @@ def main():
     if os.environ.get("DM_BENCH_DEBUG"):
         print("step ms:", [round(t, 2) for t in times], "kernel ms:", [round(sum(s["ms_count"]) + sum(s["ms_write"]), 2) for s in stats], file=sys.stderr)
     local_ms = float(sum(times))
-    t = torch.tensor([local_ms, float(count)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([local_ms, float(count)], dtype=torch.float64, device=coll_dev)
     if dist_on:
         mx = t.clone()
         tdist.all_reduce(mx, op=tdist.ReduceOp.MAX)
@@ -322,7 +331,7 @@ def main():
         b.record(stream)
         barrier()
         ems = a.elapsed_time(b)
-        t2 = torch.tensor([ems, float(ecount)], dtype=torch.float64, device="cuda")
+        t2 = torch.tensor([ems, float(ecount)], dtype=torch.float64, device=coll_dev)
         if dist_on:
             m2 = t2.clone()
             tdist.all_reduce(m2, op=tdist.ReduceOp.MAX)
