@@ -187,6 +187,10 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--rebalance", type=int, default=-1,
+                    help="N>1: exchange the frontier at this plan level by estimated work "
+                         "(NCCL all-to-all, dist.match_rebalanced); -1 = auto (level 1 for "
+                         "skewed graphs), 0 = static seed sharding only")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args, args.workload)
@@ -224,7 +228,7 @@ def main():
     off, _ = G.csr()
     cuts = equal_work_cuts(off, world)
     seed = (cuts[rank], cuts[rank + 1])
-    plan = dm.Plan(k, pe)
+    plan = dm.Plan(k, pe, stats=G.stats(count_only=True))   # the plan dm_match builds
     flush = torch.empty(int(300e6) // 4, dtype=torch.int32, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -232,7 +236,22 @@ def main():
             tdist.barrier()
         torch.cuda.synchronize()
 
+    rebalance_step = args.rebalance
+    if rebalance_step < 0:
+        rebalance_step = 1 if (dist_on and G.max_degree > 64 and plan.num_steps > 1) else 0
+    if rebalance_step >= plan.num_steps:
+        rebalance_step = 0
+
+    class _R:
+        def __init__(self, count, stats):
+            self.count, self.stats = count, stats
+
     def one(profile=False):
+        if dist_on and rebalance_step > 0:
+            from paper_2508_21287_b200.dist import rebalance_rows
+            fr = G.match_prefix(k, pe, rebalance_step, seed_range=seed, stream=stream)
+            mine = rebalance_rows(fr.rows_tensor(), fr.work_tensor(), rank=rank, world=world)
+            return G.match_resume(k, pe, rebalance_step, mine, stream=stream, profile=profile)
         return G.match(k, pe, seed_range=seed, stream=stream, profile=profile)
 
     for _ in range(max(3, args.warmup)):
@@ -356,7 +375,9 @@ def main():
                           "pattern_vertices": k, "mode": "count (monomorphism)",
                           "motifs": "M3-O,M3,M2", "plan_steps": plan.num_steps,
                           "l2_flush": "300 MB buffer written between timed steps",
-                          "parallelism": f"seed-shard x{world} (replicated graph)",
+                          "parallelism": f"seed-shard x{world} (replicated graph)" +
+                          (f", all-to-all frontier rebalance at level {rebalance_step}"
+                           if dist_on and rebalance_step > 0 else ""),
                           "prep_ms_graph_create": prep_s * 1e3},
                "roofline": roof, "cpu_baseline": cpu,
                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,

@@ -46,6 +46,7 @@ extern "C" {
 typedef struct dm_graph dm_graph;   /* device CSR of G_d (Res(M2), both orientations) */
 typedef struct dm_result dm_result; /* count + optional canonical host table + stats   */
 typedef struct dm_plan dm_plan;     /* host join program (decomposition + steps)       */
+typedef struct dm_frontier dm_frontier; /* a materialized partial-embedding level (device) */
 
 typedef enum {
   DM_OK = 0,
@@ -128,6 +129,10 @@ DM_API int32_t dm_graph_num_vertices(const dm_graph *g);
 DM_API int64_t dm_graph_num_arcs(const dm_graph *g);  /* 2 |E_d| after dedup / self-loop removal */
 DM_API int32_t dm_graph_max_degree(const dm_graph *g);
 DM_API int32_t dm_graph_device(const dm_graph *g);
+/* Statistics the planner's cost model uses: sum of squared degrees and the triangle-closure
+ * probability sampled on 4,096 arcs at creation (pass them to dm_plan_create_ex to reproduce
+ * the plan dm_match builds). */
+DM_API dm_status dm_graph_stats(const dm_graph *g, double *sum_d2, double *closure);
 /* Device pointers of the CSR (owned by g, valid until dm_graph_destroy). */
 DM_API dm_status dm_graph_device_csr(const dm_graph *g, const int64_t **d_off, const int32_t **d_adj);
 /* Copy the CSR to host buffers off_out[n+1] and adj_out[num_arcs] (either may be NULL). */
@@ -154,6 +159,33 @@ DM_API int32_t dm_result_width(const dm_result *r);          /* = k             
 DM_API const int32_t *dm_result_rows(const dm_result *r);    /* host table or NULL (count only)     */
 DM_API dm_status dm_result_stats(const dm_result *r, dm_match_stats *out);
 DM_API void dm_result_free(dm_result *r);
+
+/*
+ * Step-level entry points for multi-GPU frontier rebalancing (C2 all-to-all).
+ * The plan dm_match builds is deterministic for (g, pattern, opt), so a level produced by
+ * dm_match_prefix can be exchanged between ranks and finished by dm_match_resume with the same
+ * arguments.
+ *   dm_match_prefix: run join steps [0, upto_step) for the seed range in opt and return level
+ *       `upto_step` (1 <= upto_step < num_steps) as device rows: int32 [rows][stride],
+ *       stride = dm_frontier_stride (16-byte padded, padding -1), columns in plan (match) order,
+ *       plus a per-row uint64 work estimate of the next step (anchor degree ^ new vertices).
+ *       The dm_frontier owns both device buffers (dm_frontier_free).
+ *   dm_match_resume: finish the plan from level `from_step` given device rows in that layout
+ *       (d_rows is read only; caller keeps ownership); result as dm_match.  Disjoint row sets
+ *       give disjoint results, so the per-rank counts / tables of a repartitioned level sum up.
+ * Errors: DM_ERR_ARG (step out of range, NULL rows with rows > 0) plus dm_match's.
+ */
+DM_API dm_status dm_match_prefix(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                                 const dm_match_opts *opt, int32_t upto_step, dm_frontier **out);
+DM_API int64_t dm_frontier_rows(const dm_frontier *f);
+DM_API int32_t dm_frontier_width(const dm_frontier *f);
+DM_API int32_t dm_frontier_stride(const dm_frontier *f);
+DM_API const int32_t *dm_frontier_device_rows(const dm_frontier *f);
+DM_API const uint64_t *dm_frontier_device_work(const dm_frontier *f);
+DM_API void dm_frontier_free(dm_frontier *f);
+DM_API dm_status dm_match_resume(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                                 const dm_match_opts *opt, int32_t from_step, const int32_t *d_rows,
+                                 int64_t rows, dm_result **out);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 DM_API const char *dm_last_error(void);

@@ -75,11 +75,13 @@ _lib = None
 # every symbol include/deltamotif.h declares (checked by tests/test_abi.py)
 EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_destroy",
            "dm_graph_num_vertices", "dm_graph_num_arcs", "dm_graph_max_degree",
-           "dm_graph_device", "dm_graph_device_csr", "dm_graph_copy_csr", "dm_match",
+           "dm_graph_device", "dm_graph_stats", "dm_graph_device_csr", "dm_graph_copy_csr", "dm_match",
            "dm_result_count", "dm_result_width", "dm_result_rows", "dm_result_stats",
            "dm_result_free", "dm_last_error", "dm_plan_create", "dm_plan_create_ex", "dm_plan_destroy",
            "dm_plan_num_slices", "dm_plan_slice", "dm_plan_num_steps", "dm_plan_first_vertex",
-           "dm_plan_describe"]
+           "dm_plan_describe", "dm_match_prefix", "dm_frontier_rows", "dm_frontier_width",
+           "dm_frontier_stride", "dm_frontier_device_rows", "dm_frontier_device_work",
+           "dm_frontier_free", "dm_match_resume"]
 
 
 def lib():
@@ -102,6 +104,7 @@ def lib():
         "dm_graph_num_arcs": (c.c_int64, [P]),
         "dm_graph_max_degree": (c.c_int32, [P]),
         "dm_graph_device": (c.c_int32, [P]),
+        "dm_graph_stats": (c.c_int, [P, c.POINTER(c.c_double), c.POINTER(c.c_double)]),
         "dm_graph_device_csr": (c.c_int, [P, c.POINTER(P), c.POINTER(P)]),
         "dm_graph_copy_csr": (c.c_int, [P, P, P]),
         "dm_match": (c.c_int, [P, c.c_int32, P, c.c_int64, c.POINTER(_Opts), c.POINTER(P)]),
@@ -123,6 +126,16 @@ def lib():
         "dm_plan_num_steps": (c.c_int32, [P]),
         "dm_plan_first_vertex": (c.c_int32, [P]),
         "dm_plan_describe": (c.c_int64, [P, c.c_char_p, c.c_int64]),
+        "dm_match_prefix": (c.c_int, [P, c.c_int32, P, c.c_int64, c.POINTER(_Opts), c.c_int32,
+                                      c.POINTER(P)]),
+        "dm_frontier_rows": (c.c_int64, [P]),
+        "dm_frontier_width": (c.c_int32, [P]),
+        "dm_frontier_stride": (c.c_int32, [P]),
+        "dm_frontier_device_rows": (P, [P]),
+        "dm_frontier_device_work": (P, [P]),
+        "dm_frontier_free": (None, [P]),
+        "dm_match_resume": (c.c_int, [P, c.c_int32, P, c.c_int64, c.POINTER(_Opts), c.c_int32, P,
+                                      c.c_int64, c.POINTER(P)]),
     }
     for name, (rt, args) in sig.items():
         f = getattr(L, name)
@@ -226,6 +239,44 @@ def _stats_dict(s: _Stats) -> dict:
     }
 
 
+class _CudaArray:
+    """Minimal __cuda_array_interface__ view of library-owned device memory (for torch.as_tensor)."""
+
+    def __init__(self, ptr, shape, typestr, owner):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr or 0), False), "version": 3,
+                                         "strides": None}
+        self._owner = owner
+
+
+class Frontier:
+    """A materialized level (dm_match_prefix): device rows [rows][stride] int32 in plan column
+    order plus a per-row uint64 work estimate.  Owns the device buffers."""
+
+    def __init__(self, h):
+        L = lib()
+        self._h = h
+        self.rows = int(L.dm_frontier_rows(h))
+        self.width = int(L.dm_frontier_width(h))
+        self.stride = int(L.dm_frontier_stride(h))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.dm_frontier_free(self._h)
+            self._h = None
+
+    def rows_tensor(self, device=None):
+        """torch view of the device rows (valid while this Frontier lives)."""
+        import torch
+        p = lib().dm_frontier_device_rows(self._h)
+        return torch.as_tensor(_CudaArray(p, (self.rows, self.stride), "<i4", self), device=device)
+
+    def work_tensor(self, device=None):
+        import torch
+        p = lib().dm_frontier_device_work(self._h)
+        return torch.as_tensor(_CudaArray(p, (self.rows,), "<i8", self), device=device)
+
+
 # ------------------------------------------------------------------------------- graphs
 class Graph:
     """Device-resident data graph (dm_graph_create): Res(M2) as a sorted CSR on `device`."""
@@ -259,6 +310,13 @@ class Graph:
     def max_degree(self) -> int:
         return lib().dm_graph_max_degree(self._h)
 
+    def stats(self, count_only: bool = True) -> dict:
+        """Cost-model statistics (for Plan(..., stats=g.stats()) == the plan dm_match uses)."""
+        a, b = ctypes.c_double(), ctypes.c_double()
+        _check(lib().dm_graph_stats(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return dict(n=max(self.n, 2), arcs=self.num_arcs, sum_d2=a.value, closure=b.value,
+                    max_degree=self.max_degree, count_only=count_only)
+
     def csr(self):
         """(off int64[n+1], adj int32[arcs]) copied to the host."""
         off = np.zeros(self.n + 1, dtype=np.int64)
@@ -266,14 +324,8 @@ class Graph:
         _check(lib().dm_graph_copy_csr(self._h, off.ctypes.data, adj.ctypes.data))
         return off, adj[: self.num_arcs]
 
-    def match(self, k: int, p_edges, *, mode: str = "mono", output: str = "count",
-              motifs="all", seed_range=None, stream=None, profile: bool = False,
-              mem_budget: int = 0, row_budget: int = 0) -> Result:
-        """dm_match: embeddings of the pattern (k, p_edges).  output in {"count", "table",
-        "both"}; seed_range=(b, e) restricts f(first plan vertex) to [b, e); stream is a
-        torch.cuda.Stream / raw cudaStream_t int (None = legacy default stream)."""
+    def _opts(self, mode, output, motifs, seed_range, stream, profile, mem_budget, row_budget):
         L = lib()
-        pe = _edges_arr(p_edges)
         o = _Opts()
         L.dm_match_opts_init(ctypes.byref(o))
         o.mode = DM_INDUCED if mode == "induced" else DM_MONO
@@ -286,9 +338,34 @@ class Graph:
             o.seed_begin, o.seed_end = int(seed_range[0]), int(seed_range[1])
         if stream is not None:
             o.cuda_stream = int(getattr(stream, "cuda_stream", stream))
+        return o
+
+    def match_prefix(self, k: int, p_edges, upto_step: int, *, mode: str = "mono",
+                     output: str = "count", motifs="all", seed_range=None, stream=None) -> Frontier:
+        """dm_match_prefix: run join steps [0, upto_step) and return level upto_step."""
+        pe = _edges_arr(p_edges)
+        o = self._opts(mode, output, motifs, seed_range, stream, False, 0, 0)
+        h = ctypes.c_void_p()
+        _check(lib().dm_match_prefix(self._h, int(k), pe.ctypes.data if pe.size else None,
+                                     pe.shape[0], ctypes.byref(o), int(upto_step), ctypes.byref(h)))
+        return Frontier(h)
+
+    def match_resume(self, k: int, p_edges, from_step: int, rows, *, mode: str = "mono",
+                     output: str = "count", motifs="all", stream=None, profile: bool = False) -> Result:
+        """dm_match_resume: finish the plan from a level given as a CUDA int32 tensor
+        [rows][stride] (plan column order)."""
+        pe = _edges_arr(p_edges)
+        o = self._opts(mode, output, motifs, None, stream, profile, 0, 0)
+        n = int(rows.shape[0]) if rows is not None else 0
+        ptr = rows.data_ptr() if n else None
         r = ctypes.c_void_p()
-        _check(L.dm_match(self._h, int(k), pe.ctypes.data if pe.size else None, pe.shape[0],
-                          ctypes.byref(o), ctypes.byref(r)))
+        _check(lib().dm_match_resume(self._h, int(k), pe.ctypes.data if pe.size else None,
+                                     pe.shape[0], ctypes.byref(o), int(from_step), ptr, n,
+                                     ctypes.byref(r)))
+        return self._result(r, k, output)
+
+    def _result(self, r, k, output) -> Result:
+        L = lib()
         try:
             cnt = int(L.dm_result_count(r))
             rows = None
@@ -303,3 +380,16 @@ class Graph:
             return Result(cnt, rows, _stats_dict(st))
         finally:
             L.dm_result_free(r)
+
+    def match(self, k: int, p_edges, *, mode: str = "mono", output: str = "count",
+              motifs="all", seed_range=None, stream=None, profile: bool = False,
+              mem_budget: int = 0, row_budget: int = 0) -> Result:
+        """dm_match: embeddings of the pattern (k, p_edges).  output in {"count", "table",
+        "both"}; seed_range=(b, e) restricts f(first plan vertex) to [b, e); stream is a
+        torch.cuda.Stream / raw cudaStream_t int (None = legacy default stream)."""
+        pe = _edges_arr(p_edges)
+        o = self._opts(mode, output, motifs, seed_range, stream, profile, mem_budget, row_budget)
+        r = ctypes.c_void_p()
+        _check(lib().dm_match(self._h, int(k), pe.ctypes.data if pe.size else None, pe.shape[0],
+                              ctypes.byref(o), ctypes.byref(r)))
+        return self._result(r, k, output)

@@ -284,6 +284,14 @@ int64_t dm_graph_num_arcs(const dm_graph *g) { return g ? g->arcs : -1; }
 int32_t dm_graph_max_degree(const dm_graph *g) { return g ? g->max_deg : -1; }
 int32_t dm_graph_device(const dm_graph *g) { return g ? g->device : -1; }
 
+dm_status dm_graph_stats(const dm_graph *g, double *sum_d2, double *closure) {
+  dm::clear_error();
+  if (!g) return dm::fail(DM_ERR_ARG, "graph is NULL");
+  if (sum_d2) *sum_d2 = g->sum_d2;
+  if (closure) *closure = g->closure;
+  return DM_OK;
+}
+
 dm_status dm_graph_device_csr(const dm_graph *g, const int64_t **d_off, const int32_t **d_adj) {
   dm::clear_error();
   if (!g) return dm::fail(DM_ERR_ARG, "graph is NULL");

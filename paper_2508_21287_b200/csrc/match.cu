@@ -24,6 +24,14 @@
 
 #include "dm_device.cuh"
 
+struct dm_frontier {
+  int device = 0;
+  int32_t *rows = nullptr;            // device, [n][row_stride(w)]
+  uint64_t n = 0;
+  int32_t w = 0;
+  unsigned long long *work = nullptr;  // device, [n]
+};
+
 struct dm_result {
   uint64_t count = 0;
   int32_t k = 0;
@@ -132,6 +140,9 @@ struct Ctx {
   int32_t *d_res = nullptr;             // table mode: rows in column (match) order
   uint64_t res_rows = 0, res_cap = 0;
   std::vector<double> ratio;            // observed output/input rows per step (capacity estimate)
+  int stop_at = -1;                     // dm_match_prefix: collect level `stop_at` instead of running it
+  int32_t *d_front = nullptr;           //   collected rows (stride row_stride(w))
+  uint64_t front_rows = 0, front_cap = 0;
   dm_match_stats st;
   Prof prof;
 };
@@ -203,6 +214,26 @@ dm_status write_tiles(Ctx &c, int si, const StepIO &base_io, const uint64_t *d_e
 
 dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t seed_base) {
   if (in_rows <= 0) return DM_OK;
+  if (si == c.stop_at) {  // dm_match_prefix: append this (chunk of the) level to the collector
+    const int Win = row_stride(c.dsteps[(size_t)si].in_w);
+    if (c.front_rows + (uint64_t)in_rows > c.front_cap) {
+      uint64_t cap = std::max<uint64_t>(c.front_rows + (uint64_t)in_rows, c.front_cap * 2);
+      int32_t *p = nullptr;
+      CK(cudaMallocAsync((void **)&p, sizeof(int32_t) * (size_t)cap * Win, c.s), "frontier allocation");
+      if (c.front_rows)
+        CK(cudaMemcpyAsync(p, c.d_front, sizeof(int32_t) * (size_t)c.front_rows * Win,
+                           cudaMemcpyDeviceToDevice, c.s),
+           "frontier copy");
+      if (c.d_front) cudaFreeAsync(c.d_front, c.s);
+      c.d_front = p;
+      c.front_cap = cap;
+    }
+    CK(cudaMemcpyAsync(c.d_front + (size_t)c.front_rows * Win, in, sizeof(int32_t) * (size_t)in_rows * Win,
+                       cudaMemcpyDeviceToDevice, c.s),
+       "frontier copy");
+    c.front_rows += (uint64_t)in_rows;
+    return DM_OK;
+  }
   const int nsteps = (int)c.plan->steps.size();
   const DevStep &D = c.dsteps[(size_t)si];
   const bool last = si == nsteps - 1;
@@ -417,9 +448,37 @@ void configure_pool(int device) {
   done[device] = true;
 }
 
+// Per-row work estimate of the next step (for frontier rebalancing): degree of the first new
+// vertex's anchor key raised to the number of new vertices.
+__global__ void k_row_work(const int32_t *__restrict__ rows, int64_t n, int stride, const DevStep st,
+                           const int64_t *__restrict__ off, unsigned long long *__restrict__ work) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t *row = rows + i * stride;
+    unsigned long long best = ~0ull;
+    for (int t = 0; t < st.n_nbr[0]; ++t) {
+      const int32_t v = row[st.nbr[0][t]];
+      const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+      best = d < best ? d : best;
+    }
+    unsigned long long wk = 1;
+    for (int j = 0; j < st.n_new; ++j) wk *= (best + 1);
+    work[i] = wk;
+  }
+}
+
+struct FrontierOut {
+  int32_t *rows = nullptr;
+  uint64_t n = 0;
+  int w = 0;
+  unsigned long long *work = nullptr;
+};
+
 dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
-                     const dm_match_opts *opt_in, dm_result **out) {
-  if (!g || !out) return fail(DM_ERR_ARG, "graph/out is NULL");
+                     const dm_match_opts *opt_in, dm_result **out, int stop_at = -1,
+                     FrontierOut *fout = nullptr, int from_step = 0,
+                     const int32_t *from_rows = nullptr, int64_t from_n = 0) {
+  if (!g || (!out && !fout)) return fail(DM_ERR_ARG, "graph/out is NULL");
   dm_match_opts opt;
   dm_match_opts_init(&opt);
   if (opt_in) opt = *opt_in;
@@ -473,6 +532,12 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   c.prof.on = (opt.flags & DM_MATCH_PROFILE) != 0;
   c.prof.s = c.s;
 
+  const int nst = (int)plan.steps.size();
+  if (stop_at >= 0 && (stop_at < 1 || stop_at >= nst))
+    return fail(DM_ERR_ARG, "upto_step must be in [1, num_steps)");
+  if (from_step != 0 && (from_step < 1 || from_step >= nst || (from_n > 0 && !from_rows)))
+    return fail(DM_ERR_ARG, "from_step must be in [1, num_steps) with device rows");
+  c.stop_at = stop_at;
   dm_result *res = new (std::nothrow) dm_result;
   if (!res) return fail(DM_ERR_OOM, "host allocation failed");
   res->k = k;
@@ -513,8 +578,26 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
       for (uint64_t i = 0; i < count; ++i) res->rows[i] = (int32_t)(sb + (int64_t)i);
     }
   } else {
-    stt = run_step(c, 0, nullptr, se - sb, sb);
-    if (stt != DM_OK) return stt;
+    if (from_step > 0) stt = run_step(c, from_step, from_rows, from_n, 0);
+    else stt = run_step(c, 0, nullptr, se - sb, sb);
+    if (stt != DM_OK) {
+      if (c.d_front) cudaFreeAsync(c.d_front, c.s);
+      return stt;
+    }
+    if (stop_at >= 0) {  // dm_match_prefix: hand the collected level over with work estimates
+      fout->rows = c.d_front;
+      fout->n = c.front_rows;
+      fout->w = plan.steps[(size_t)stop_at].in_w;
+      CK(cudaMallocAsync((void **)&fout->work, sizeof(unsigned long long) * std::max<uint64_t>(c.front_rows, 1), c.s),
+         "work allocation");
+      if (c.front_rows) {
+        k_row_work<<<grid_for((int64_t)c.front_rows), 256, 0, c.s>>>(
+            c.d_front, (int64_t)c.front_rows, row_stride(fout->w), c.dsteps[(size_t)stop_at], g->d_off, fout->work);
+        CK(cudaGetLastError(), "work kernel");
+      }
+      CK(cudaStreamSynchronize(c.s), "sync");
+      return DM_OK;
+    }
     if (c.table) {
       count = c.res_rows;
       res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count * k, 1));
@@ -561,6 +644,49 @@ dm_status dm_match(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t
                    const dm_match_opts *opt, dm_result **out) {
   dm::clear_error();
   return dm::match_impl(g, k, p_edges, pm, opt, out);
+}
+
+dm_status dm_match_prefix(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                          const dm_match_opts *opt, int32_t upto_step, dm_frontier **out) {
+  dm::clear_error();
+  if (!g || !out) return dm::fail(DM_ERR_ARG, "graph/out is NULL");
+  dm::FrontierOut fo;
+  dm_status st = dm::match_impl(g, k, p_edges, pm, opt, nullptr, upto_step, &fo);
+  if (st != DM_OK) return st;
+  dm_frontier *f = new (std::nothrow) dm_frontier;
+  if (!f) return dm::fail(DM_ERR_OOM, "host allocation failed");
+  f->device = g->device;
+  f->rows = fo.rows;
+  f->n = fo.n;
+  f->w = fo.w;
+  f->work = fo.work;
+  *out = f;
+  return DM_OK;
+}
+
+int64_t dm_frontier_rows(const dm_frontier *f) { return f ? (int64_t)f->n : -1; }
+int32_t dm_frontier_width(const dm_frontier *f) { return f ? f->w : -1; }
+int32_t dm_frontier_stride(const dm_frontier *f) { return f ? dm::row_stride(f->w) : -1; }
+const int32_t *dm_frontier_device_rows(const dm_frontier *f) { return f ? f->rows : nullptr; }
+const uint64_t *dm_frontier_device_work(const dm_frontier *f) {
+  return f ? reinterpret_cast<const uint64_t *>(f->work) : nullptr;
+}
+
+void dm_frontier_free(dm_frontier *f) {
+  if (!f) return;
+  dm::DeviceGuard dg(f->device);
+  cudaDeviceSynchronize();
+  if (f->rows) cudaFree(f->rows);
+  if (f->work) cudaFree(f->work);
+  delete f;
+}
+
+dm_status dm_match_resume(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                          const dm_match_opts *opt, int32_t from_step, const int32_t *d_rows,
+                          int64_t rows, dm_result **out) {
+  dm::clear_error();
+  if (rows < 0) return dm::fail(DM_ERR_ARG, "rows < 0");
+  return dm::match_impl(g, k, p_edges, pm, opt, out, -1, nullptr, from_step, d_rows, rows);
 }
 
 uint64_t dm_result_count(const dm_result *r) { return r ? r->count : 0; }

@@ -74,6 +74,65 @@ def match_sharded(local_match: Callable[[int, int], tuple[int, np.ndarray | None
     return total, merge_tables(parts, k)
 
 
+def rebalance_rows(rows, work, *, rank: int, world: int):
+    """Frontier rebalancing (collectives C1 + C2): every rank holds `rows`
+    ([n_r, stride] int32) with per-row work estimates `work` ([n_r] int64).  Rows are assigned
+    to ranks by their position in the global work prefix (rank order, then row order), so each
+    rank receives a contiguous 1/world share of the total work; returns this rank's rows.
+    all_gather of per-rank work totals (C1), all_to_all of row counts, all_to_all_single of the
+    rows themselves (C2).  Works with NCCL (CUDA tensors) and gloo (CPU tensors)."""
+    import torch
+    import torch.distributed as tdist
+
+    dev = rows.device
+    n = int(rows.shape[0])
+    stride = int(rows.shape[1]) if rows.dim() == 2 else 1
+    w = work.to(torch.int64)
+    tot = torch.tensor([int(w.sum().item()) if n else 0], dtype=torch.int64, device=dev)
+    tots = [torch.zeros(1, dtype=torch.int64, device=dev) for _ in range(world)]
+    tdist.all_gather(tots, tot)
+    tots = [int(t.item()) for t in tots]
+    total = sum(tots)
+    base = sum(tots[:rank])
+    if n:
+        pos = base + torch.cumsum(w, 0) - w                      # exclusive global prefix
+        dest = torch.clamp((pos * world) // max(total, 1), 0, world - 1) if total else \
+            torch.zeros(n, dtype=torch.int64, device=dev)
+        send = torch.bincount(dest, minlength=world).to(torch.int64)
+    else:
+        send = torch.zeros(world, dtype=torch.int64, device=dev)
+    recv = torch.empty_like(send)
+    tdist.all_to_all_single(recv, send)
+    send_l = [int(x) for x in send.tolist()]
+    recv_l = [int(x) for x in recv.tolist()]
+    out = torch.empty((sum(recv_l), stride), dtype=rows.dtype, device=dev)
+    src = rows.reshape(n, stride).contiguous()
+    tdist.all_to_all_single(out, src, output_split_sizes=recv_l, input_split_sizes=send_l)
+    return out
+
+
+def match_rebalanced(graph, k: int, p_edges, work_prefix, *, rank: int, world: int, step: int,
+                     stream=None, mode: str = "mono", reduce: bool = True):
+    """Count mode with a frontier exchange: run the plan to level `step` on this rank's seed
+    shard (dm_match_prefix), rebalance the level by estimated work across ranks (NCCL
+    all-to-all), finish locally (dm_match_resume) and all_reduce the count (C3)."""
+    import torch
+    import torch.distributed as tdist
+
+    cuts = equal_work_cuts(work_prefix, world)
+    fr = graph.match_prefix(k, p_edges, step, mode=mode, seed_range=(cuts[rank], cuts[rank + 1]),
+                            stream=stream)
+    rows = fr.rows_tensor()
+    work = fr.work_tensor()
+    mine = rebalance_rows(rows, work, rank=rank, world=world)
+    r = graph.match_resume(k, p_edges, step, mine, mode=mode, stream=stream)
+    if not reduce:
+        return int(r.count), int(mine.shape[0])
+    t = torch.tensor([int(r.count)], dtype=torch.int64, device=rows.device)
+    tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
+    return int(t.item()), int(mine.shape[0])
+
+
 def graph_local_match(graph, k: int, p_edges, *, output: str = "count", stream=None, **kw):
     """local_match adapter over Graph.match for match_sharded."""
     def run(b: int, e: int):

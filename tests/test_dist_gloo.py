@@ -77,3 +77,52 @@ def test_merge_tables():
     b = np.array([[1, 5]], np.int32)
     m = merge_tables([a, b, np.zeros((0, 2), np.int32)], 2)
     assert m.tolist() == [[0, 2], [1, 5], [3, 1]]
+
+
+def _rebalance_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as tdist
+    from paper_2508_21287_b200.dist import rebalance_rows
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = torch.Generator().manual_seed(100 + rank)
+        n = [37, 5, 0][rank % 3] if world == 3 else [40, 3][rank]
+        rows = torch.randint(0, 1000, (n, 4), generator=g, dtype=torch.int32)
+        rows[:, 0] = rank * 1000 + torch.arange(n, dtype=torch.int32)   # unique row ids
+        work = torch.randint(1, 50, (n,), generator=g, dtype=torch.int64)
+        got = rebalance_rows(rows, work, rank=rank, world=world)
+        # gather everything (pickled) to check conservation and balance
+        everything = [None] * world
+        tdist.all_gather_object(everything, (rows.tolist(), work.tolist(), got.tolist()))
+        idmap, before, after = {}, [], []
+        for rr, ww, gg in everything:
+            for row, wk in zip(rr, ww):
+                idmap[row[0]] = wk
+            before += [tuple(r) for r in rr]
+            after += [tuple(r) for r in gg]
+        before.sort()
+        after.sort()
+        total = sum(idmap.values())
+        mywork = sum(idmap[r[0]] for r in got.tolist())
+        maxw = max(idmap.values()) if idmap else 0
+        out.put((rank, before == after, abs(mywork - total / world) <= maxw + 1))
+    finally:
+        tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_rebalance_rows_gloo(world):
+    """C1 + C2: rows are conserved and every rank ends with ~1/world of the total work."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(ok1 and ok2 for _, ok1, ok2 in res), res

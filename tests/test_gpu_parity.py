@@ -265,6 +265,38 @@ def test_seed_ranges_partition(dm):
     assert np.array_equal(cat, full)
 
 
+def test_prefix_resume_split(dm):
+    """dm_match_prefix + dm_match_resume: a level cut into two row sets and finished separately
+    gives the full result (the multi-GPU frontier exchange contract)."""
+    import torch
+    cases = [(g.ibm_heavy_hex(6), g.path(11), False), (g.rmat(10, 16, seed=3), g.diamond(), True),
+             (g.grid_diag(20), g.ring(5), False), (g.er_gnm(300, 2000, 4), g.clique(4), False)]
+    for (n, e), (k, pe), drop in cases:
+        G = dm.Graph(n, e, drop_self_loops=drop)
+        full = G.match(k, pe, output="both")
+        nsteps = dm.Plan(k, pe, stats=G.stats(count_only=False)).num_steps
+        assert nsteps == full.stats["num_steps"]
+        assert dm.Plan(k, pe, stats=G.stats()).num_steps == G.match(k, pe).stats["num_steps"]
+        for step in range(1, max(2, nsteps)):
+            try:
+                fr = G.match_prefix(k, pe, step, output="both")
+            except dm.DMError:
+                continue
+            rows = fr.rows_tensor()
+            assert rows.shape == (fr.rows, fr.stride) and fr.work_tensor().shape == (fr.rows,)
+            cut = fr.rows // 3
+            a = G.match_resume(k, pe, step, rows[:cut].contiguous(), output="both")
+            b = G.match_resume(k, pe, step, rows[cut:].contiguous(), output="both")
+            assert a.count + b.count == full.count
+            cat = np.concatenate([a.rows, b.rows])
+            cat = cat[np.lexsort(cat.T[::-1])]
+            assert np.array_equal(cat, full.rows)
+            c = G.match_resume(k, pe, step, rows, output="both")
+            assert c.count == full.count
+    with pytest.raises(dm.DMError):
+        G.match_prefix(k, pe, 0)
+
+
 def test_chunking_and_budgets(dm):
     n, e = g.ibm_heavy_hex(10)
     G = dm.Graph(n, e)
