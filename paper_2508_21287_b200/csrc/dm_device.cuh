@@ -47,7 +47,7 @@ struct DeviceGuard {
 constexpr int kStepThreads = 256;   // threads per CTA
 constexpr int kTileRows = 256;      // frontier rows per CTA tile
 constexpr int kSurvBuf = 1024;      // survivors staged in shared memory per CTA
-constexpr int kRowSlotsMax = 8;     // row-serial kernel: max survivor slots per frontier row
+constexpr int kRowSlotsMax = 4;     // row-serial kernel: max survivor slots per frontier row
 constexpr int kRowSerialDeg1 = 16;  // row-serial kernel for 1-vertex steps if max degree <= 16
 constexpr int kRowSerialDeg2 = 4;   //   ... and for 2-vertex steps if max degree <= 4
 constexpr int kPairSmem = 1024;     // shared-key pair kernel: per-warp list in shared memory

@@ -34,6 +34,7 @@
 //                 record themselves and are re-run by the host with kModeWrite.
 #include <cub/cub.cuh>
 
+#include <map>
 #include <mutex>
 
 #include "dm_device.cuh"
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(kStepThreads)
 // that overflows its slots marks the tile unwritten and the host re-runs it with the general
 // kernel (kModeWrite).  Output order is identical to k_step (row, then candidate order).
 template <int MODE, int NQ, bool ELL>
-__global__ void __launch_bounds__(kStepThreads)
+__global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ? 64 : 48)
     k_rows(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -774,68 +775,62 @@ __global__ void __launch_bounds__(kStepThreads)
     }
     ++ns;
   };
-  if (MODE == kModeCount && ELL && st.n_new > 2) {
-    if (tid < nrows) {
-      int32_t x[kMaxNew] = {-1, -1, -1, -1};
-      const int32_t *row = rows + tid * ss;
+  // all survivors of this thread's row, in candidate order
+  auto enumerate = [&](auto &&on_survivor, uint32_t &n_cand, uint32_t &n_probe) {
+    const int32_t *row = rows + tid * ss;
+    if (ELL) {
+      // max degree <= 4: candidate lists are single int4 loads (sorted, -1 padded)
+      const int4 *ell = reinterpret_cast<const int4 *>(io.ell);
       unsigned long long bloom = 0;
       for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
-      ns = (int)dfs_ell<0, NQ>(st, row, w, ws, bloom, x, reinterpret_cast<const int4 *>(io.ell),
-                               my_cand, my_probe);
-    }
-  } else if (tid < nrows && ELL) {
-    // max degree <= 4: candidate lists are single int4 loads (sorted, -1 padded)
-    const int32_t *row = rows + tid * ss;
-    const int4 *ell = reinterpret_cast<const int4 *>(io.ell);
-    unsigned long long bloom = 0;
-    for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
-    int4 na;
-    const int ac = pick_anchor_ell(st, 0, row, w, 0, ell, na);
+      int4 na;
+      const int ac = pick_anchor_ell(st, 0, row, w, 0, ell, na);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int32_t x0 = ell_at(na, i);
-      if (x0 < 0) break;
-      ++my_cand;
-      if (!accept_ell<NQ>(st, 0, row, w, ws, bloom, 0, x0, ac, ell, my_probe)) continue;
-      if (st.n_new == 1) {
-        record(x0, -1);
-        continue;
-      }
-      int4 nb;
-      const int bc = pick_anchor_ell(st, 1, row, w, x0, ell, nb);
+      for (int i = 0; i < 4; ++i) {
+        const int32_t x0 = ell_at(na, i);
+        if (x0 < 0) break;
+        ++n_cand;
+        if (!accept_ell<NQ>(st, 0, row, w, ws, bloom, 0, x0, ac, ell, n_probe)) continue;
+        if (st.n_new == 1) {
+          on_survivor(x0, -1);
+          continue;
+        }
+        int4 nb;
+        const int bc = pick_anchor_ell(st, 1, row, w, x0, ell, nb);
 #pragma unroll
-      for (int i1 = 0; i1 < 4; ++i1) {
-        const int32_t x1 = ell_at(nb, i1);
-        if (x1 < 0) break;
-        ++my_cand;
-        if (accept_ell<NQ>(st, 1, row, w, ws, bloom, x0, x1, bc, ell, my_probe)) record(x0, x1);
+        for (int i1 = 0; i1 < 4; ++i1) {
+          const int32_t x1 = ell_at(nb, i1);
+          if (x1 < 0) break;
+          ++n_cand;
+          if (accept_ell<NQ>(st, 1, row, w, ws, bloom, x0, x1, bc, ell, n_probe)) on_survivor(x0, x1);
+        }
+      }
+    } else {
+      int32_t av;
+      int64_t ad;
+      const int ac = pick_anchor(st, 0, row, w, 0, off, av, ad);
+      const int64_t e0 = __ldg(off + av);
+      for (int64_t e = e0; e < e0 + ad; ++e) {
+        const int32_t x0 = __ldg(adj + e);
+        ++n_cand;
+        if (!accept<NQ>(st, 0, row, w, ws, 0, x0, ac, off, adj, n_probe)) continue;
+        if (st.n_new == 1) {
+          on_survivor(x0, -1);
+          continue;
+        }
+        int32_t bv;
+        int64_t bd;
+        const int bc = pick_anchor(st, 1, row, w, x0, off, bv, bd);
+        const int64_t f0 = __ldg(off + bv);
+        for (int64_t f = f0; f < f0 + bd; ++f) {
+          const int32_t x1 = __ldg(adj + f);
+          ++n_cand;
+          if (accept<NQ>(st, 1, row, w, ws, x0, x1, bc, off, adj, n_probe)) on_survivor(x0, x1);
+        }
       }
     }
-  } else if (tid < nrows) {
-    const int32_t *row = rows + tid * ss;
-    int32_t av;
-    int64_t ad;
-    const int ac = pick_anchor(st, 0, row, w, 0, off, av, ad);
-    const int64_t e0 = __ldg(off + av);
-    for (int64_t e = e0; e < e0 + ad; ++e) {
-      const int32_t x0 = __ldg(adj + e);
-      ++my_cand;
-      if (!accept<NQ>(st, 0, row, w, ws, 0, x0, ac, off, adj, my_probe)) continue;
-      if (st.n_new == 1) {
-        record(x0, -1);
-        continue;
-      }
-      int32_t bv;
-      int64_t bd;
-      const int bc = pick_anchor(st, 1, row, w, x0, off, bv, bd);
-      const int64_t f0 = __ldg(off + bv);
-      for (int64_t f = f0; f < f0 + bd; ++f) {
-        const int32_t x1 = __ldg(adj + f);
-        ++my_cand;
-        if (accept<NQ>(st, 1, row, w, ws, x0, x1, bc, off, adj, my_probe)) record(x0, x1);
-      }
-    }
-  }
+  };
+  if (tid < nrows) enumerate(record, my_cand, my_probe);
   // statistics and count-mode totals: CTA reduction, one atomic per CTA on slot tile % 64
   if (io.stats || MODE == kModeCount) {
     unsigned long long v3[3] = {my_cand, my_probe, (unsigned long long)ns};
@@ -862,13 +857,83 @@ __global__ void __launch_bounds__(kStepThreads)
     const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
     if (tid == 0) {
       atomicAdd(io.ctrl + 2, (unsigned long long)agg);
-      const bool fits = !any_ovf && excl + (unsigned long long)agg <= io.cap;
+      const bool fits = excl + (unsigned long long)agg <= io.cap;
       if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
       s_bc = fits ? excl : ~0ull;
     }
   }
   __syncthreads();
-  if (s_bc != ~0ull) flush_rows(rows, nullptr, sv_x, map, S, w, st.n_new, agg, io.out, (int64_t)s_bc);
+  if (s_bc == ~0ull) return;
+  if (!any_ovf) {
+    flush_rows(rows, nullptr, sv_x, map, S, w, st.n_new, agg, io.out, (int64_t)s_bc);
+    return;
+  }
+  // a row overflowed its slots: every thread re-enumerates its row and writes its survivors
+  // directly at their final positions (same order, uncoalesced; rare)
+  if (tid < nrows && ns > 0) {
+    const int32_t *row = rows + tid * ss;
+    const int nq = row_stride(w + st.n_new) >> 2, nqs = ws >> 2, qw = w >> 2;
+    int4 *dst = reinterpret_cast<int4 *>(io.out) + ((int64_t)s_bc + pos) * nq;
+    uint32_t dc = 0, dp = 0;
+    enumerate(
+        [&](int32_t x0, int32_t x1) {
+          for (int q = 0; q < nq; ++q) {
+            int4 v = q < nqs ? reinterpret_cast<const int4 *>(row)[q] : make_int4(-1, -1, -1, -1);
+            if (q == qw || q == qw + 1) {
+              int32_t t4[4] = {v.x, v.y, v.z, v.w};
+              for (int c = 0; c < 4; ++c) {
+                const int col = 4 * q + c;
+                if (col == w) t4[c] = x0;
+                if (col == w + 1 && st.n_new == 2) t4[c] = x1;
+              }
+              v = make_int4(t4[0], t4[1], t4[2], t4[3]);
+            }
+            dst[q] = v;
+          }
+          dst += nq;
+        },
+        dc, dp);
+  }
+}
+
+
+// Deep count-only last step (3-4 new vertices, ELL graphs): tile -> smem, one thread per row,
+// depth-first enumeration (dfs_ell), CTA-reduced counters.
+template <int NQ>
+__global__ void __launch_bounds__(kStepThreads)
+    k_deep(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+           const int32_t *__restrict__ adj) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t s_bar;
+  const int w = st.in_w, ws = row_stride(w), ss = smem_stride(w);
+  const int tid = threadIdx.x;
+  const int64_t tile = io.block_begin + blockIdx.x;
+  const int64_t r0 = tile * kTileRows;
+  if (r0 >= io.in_rows) return;
+  const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
+  int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
+  load_tile(rows, ss, ws, io, r0, nrows, &s_bar);
+  uint32_t my_cand = 0, my_probe = 0;
+  unsigned ns = 0;
+  if (tid < nrows) {
+    int32_t x[kMaxNew] = {-1, -1, -1, -1};
+    const int32_t *row = rows + tid * ss;
+    unsigned long long bloom = 0;
+    for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
+    ns = dfs_ell<0, NQ>(st, row, w, ws, bloom, x, reinterpret_cast<const int4 *>(io.ell), my_cand,
+                        my_probe);
+  }
+  unsigned long long v3[3] = {my_cand, my_probe, ns};
+  block_sum3(v3);
+  if (tid == 0) {
+    const int slot = (int)(tile & (kAccSlots - 1));
+    if (io.stats) {
+      atomicAdd(io.stats + slot, v3[0]);
+      atomicAdd(io.stats + kAccSlots + slot, v3[1]);
+    }
+    if (io.block_cnt) io.block_cnt[tile] = v3[2];
+    if (io.total && v3[2]) atomicAdd(io.total + slot, v3[2]);
+  }
 }
 
 size_t rows_smem_bytes(int in_w, bool stage, int slots) {
@@ -877,7 +942,8 @@ size_t rows_smem_bytes(int in_w, bool stage, int slots) {
   return b;
 }
 
-// survivor slots per row for the row-serial kernel: min(max_degree^n_new, kRowSlotsMax)
+// survivor slots per row for the row-serial kernel: min(max_degree^n_new, kRowSlotsMax); a row
+// with more survivors makes its tile fall back to direct writes
 int row_slots(const DevStep &st, const dm_graph &g) {
   int64_t d = g.max_deg < 1 ? 1 : g.max_deg;
   int64_t s = st.n_new == 1 ? d : d * d;
@@ -1038,23 +1104,36 @@ __global__ void k_status_to_excl(const unsigned long long *__restrict__ status, 
     excl[t] = t == 0 ? 0 : (status[t - 1] & kValueMask);
 }
 
-// Raise the dynamic shared-memory limit of a kernel once per (device, kernel) growth.
+// Raise the dynamic shared-memory limit (and prefer the maximum carveout) of a kernel once per
+// (device, kernel) growth.  `which` is unused (kept for call-site readability).
 cudaError_t prep(const void *fn, int which, size_t smem) {
+  (void)which;
   static std::mutex mu;
-  static size_t configured[64][96] = {};
+  static std::map<std::pair<int, const void *>, size_t> configured;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   std::lock_guard<std::mutex> lk(mu);
-  if (dev < 64 && configured[dev][which] >= smem) return cudaSuccess;
+  auto key = std::make_pair(dev, fn);
+  auto it = configured.find(key);
+  if (it != configured.end() && it->second >= smem) return cudaSuccess;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess && dev < 64) configured[dev][which] = smem;
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess) configured[key] = smem;
   return e;
 }
 
 template <int MODE, int NQ>
 cudaError_t launch_rows_nq(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
                            size_t smem, cudaStream_t s) {
+  if (MODE == kModeCount && g.d_ell && st.n_new > 2) {
+    StepIO io2 = io;
+    io2.ell = g.d_ell;
+    cudaError_t e = prep((const void *)k_deep<NQ>, 90 + NQ % 6, smem);
+    if (e != cudaSuccess) return e;
+    k_deep<NQ><<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);
+    return cudaGetLastError();
+  }
   if (g.d_ell) {
     StepIO io2 = io;
     io2.ell = g.d_ell;
