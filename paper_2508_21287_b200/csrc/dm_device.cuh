@@ -83,8 +83,8 @@ struct StepIO {
   unsigned long long *total;  // count pass: [tile % kAccSlots] += survivors (nullptr -> skip)
   unsigned long long *stats;  // [slot] += candidates, [kAccSlots + slot] += probes (or nullptr)
   unsigned long long *status; // single pass: look-back status word per tile (zeroed)
-  unsigned long long *ctrl;   // single pass: [0] tile counter (0), [1] first unwritten tile
-                              //   (init = #tiles), [2] += survivors
+  unsigned long long *ctrl;   // single pass: [0] tile counter, [1] max(#tiles - unwritten tile),
+                              //   [2] += survivors (all zero-initialised)
   uint64_t cap;               // single pass: output capacity in rows
   int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
   const int32_t *ell;         // row-serial kernel: ELL adjacency (max degree <= 4) or nullptr

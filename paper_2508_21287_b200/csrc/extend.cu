@@ -383,6 +383,9 @@ __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *ro
 }
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ inline long long ntiles_of(const StepIO &io) {
+  return (io.in_rows + kTileRows - 1) / kTileRows;
+}
 
 struct SmemLayout {
   int32_t *rows;     // [kTileRows][ws] the tile exactly as stored in global memory
@@ -711,7 +714,7 @@ __global__ void __launch_bounds__(kStepThreads)
     if (tid == 0) {
       atomicAdd(io.ctrl + 2, (unsigned long long)agg);
       const bool fits = !ovf && excl + (unsigned long long)agg <= io.cap;
-      if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
+      if (!fits) atomicMax(io.ctrl + 1, (unsigned long long)(ntiles_of(io) - tile));
       s_bc = fits ? excl : ~0ull;
     }
   }
@@ -858,7 +861,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
     if (tid == 0) {
       atomicAdd(io.ctrl + 2, (unsigned long long)agg);
       const bool fits = excl + (unsigned long long)agg <= io.cap;
-      if (!fits) atomicMin(io.ctrl + 1, (unsigned long long)tile);
+      if (!fits) atomicMax(io.ctrl + 1, (unsigned long long)(ntiles_of(io) - tile));
       s_bc = fits ? excl : ~0ull;
     }
   }

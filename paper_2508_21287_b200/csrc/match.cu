@@ -17,6 +17,11 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -78,6 +83,37 @@ int grid_for(int64_t work) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 16));
 }
 
+// Per-thread pinned host scratch for the small per-step readbacks (pageable copies would be
+// staged synchronously by the driver).
+unsigned long long *pinned_scratch() {
+  static thread_local unsigned long long *p = nullptr;
+  if (!p && cudaMallocHost((void **)&p, 64 * sizeof(unsigned long long)) != cudaSuccess) {
+    static thread_local unsigned long long fallback[64];
+    p = fallback;
+  }
+  return p;
+}
+
+// Per-thread pool of CUDA events for DM_MATCH_PROFILE (creation is not free).
+struct EventPool {
+  std::vector<cudaEvent_t> free;
+  cudaEvent_t get() {
+    if (free.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = free.back();
+    free.pop_back();
+    return e;
+  }
+  void put(cudaEvent_t e) { free.push_back(e); }
+};
+EventPool &event_pool() {
+  static thread_local EventPool p;
+  return p;
+}
+
 struct Prof {
   bool on = false;
   struct Ev {
@@ -92,8 +128,8 @@ struct Prof {
     if (!on) return;
     e.step = step;
     e.kind = kind;
-    cudaEventCreate(&e.a);
-    cudaEventCreate(&e.b);
+    e.a = event_pool().get();
+    e.b = event_pool().get();
     cudaEventRecord(e.a, s);
   }
   void end(Ev &e) {
@@ -110,8 +146,8 @@ struct Prof {
       if (e.kind == 0) st.ms_count[e.step] += ms;
       else if (e.kind == 1) st.ms_write[e.step] += ms;
       else st.ms_other += ms;
-      cudaEventDestroy(e.a);
-      cudaEventDestroy(e.b);
+      event_pool().put(e.a);
+      event_pool().put(e.b);
     }
     evs.clear();
     if (t0 && t1) {
@@ -119,8 +155,8 @@ struct Prof {
       cudaEventElapsedTime(&ms, t0, t1);
       st.ms_total = ms;
     }
-    if (t0) cudaEventDestroy(t0);
-    if (t1) cudaEventDestroy(t1);
+    if (t0) event_pool().put(t0);
+    if (t1) event_pool().put(t1);
     t0 = t1 = nullptr;
   }
 };
@@ -298,9 +334,9 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   DevBuf<unsigned long long> status, ctrl;
   CK(status.alloc((size_t)tiles, c.s), "status");
   CK(ctrl.alloc(3, c.s), "ctrl");
-  unsigned long long hctrl[3] = {0ull, (unsigned long long)tiles, 0ull};
   CK(cudaMemsetAsync(status.p, 0, sizeof(unsigned long long) * (size_t)tiles, c.s), "memset");
-  CK(cudaMemcpyAsync(ctrl.p, hctrl, sizeof(hctrl), cudaMemcpyHostToDevice, c.s), "H2D ctrl");
+  CK(cudaMemsetAsync(ctrl.p, 0, 3 * sizeof(unsigned long long), c.s), "memset");
+  unsigned long long *hctrl = pinned_scratch();
   io.status = status.p;
   io.ctrl = ctrl.p;
   io.cap = cap;
@@ -312,10 +348,11 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     c.prof.end(e);
     c.st.num_launches++;
   }
-  CK(cudaMemcpyAsync(hctrl, ctrl.p, sizeof(hctrl), cudaMemcpyDeviceToHost, c.s), "D2H ctrl");
+  CK(cudaMemcpyAsync(hctrl, ctrl.p, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.s),
+     "D2H ctrl");
   CK(cudaStreamSynchronize(c.s), "sync");
   const uint64_t total = hctrl[2];
-  const int64_t tstar = (int64_t)hctrl[1];
+  const int64_t tstar = hctrl[1] ? tiles - (int64_t)hctrl[1] : tiles;  // first unwritten tile
   c.st.rows_out[si] += total;
   c.ratio[(size_t)si] = (double)total / (double)in_rows;
   if (total == 0) return DM_OK;
@@ -437,6 +474,58 @@ dm_status canonicalize(Ctx &c, int32_t *host_out) {
   return DM_OK;
 }
 
+// Plans are pure functions of (pattern, motif set, mode, graph statistics): memoize them
+// (bounded map; repeated queries on a cached graph are the paper's GPU* use case).
+dm_status cached_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t motifs, int32_t mode,
+                      const PlanStats &st, Plan &out) {
+  static std::mutex mu;
+  static std::map<std::string, Plan> cache;
+  std::string key;
+  if (k >= 1 && pm >= 0 && (pm == 0 || p_edges)) {
+    char buf[160];
+    std::snprintf(buf, sizeof(buf), "%d|%d|%d|%.9g|%.9g|%.9g|%.9g|%d|%d|", k, motifs, mode, st.n,
+                  st.avg_degree, st.fwd_degree, st.closure, (int)st.count_only, st.max_degree);
+    key = buf;
+    key.append(reinterpret_cast<const char *>(p_edges), (size_t)pm * 2 * sizeof(int32_t));
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      out = it->second;
+      return DM_OK;
+    }
+  }
+  dm_status s = build_plan(k, p_edges, pm, motifs, mode, out, st);
+  if (s == DM_OK && !key.empty()) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(key, out);
+  }
+  return s;
+}
+
+// cudaMemGetInfo costs ~2 ms on this driver; refresh the per-device value at most every 200 ms
+// (the budget is a soft chunking target; allocation failures still surface as DM_ERR_OOM).
+cudaError_t cached_mem_info(int device, size_t *fr, size_t *tot) {
+  static std::mutex mu;
+  struct Entry {
+    size_t fr = 0, tot = 0;
+    std::chrono::steady_clock::time_point t;
+    bool valid = false;
+  };
+  static Entry cache[64];
+  std::lock_guard<std::mutex> lk(mu);
+  const auto now = std::chrono::steady_clock::now();
+  if (device >= 0 && device < 64 && cache[device].valid &&
+      now - cache[device].t < std::chrono::milliseconds(200)) {
+    *fr = cache[device].fr;
+    *tot = cache[device].tot;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMemGetInfo(fr, tot);
+  if (e == cudaSuccess && device >= 0 && device < 64) cache[device] = {*fr, *tot, now, true};
+  return e;
+}
+
 void configure_pool(int device) {
   static bool done[64] = {};
   if (device < 0 || device >= 64 || done[device]) return;
@@ -479,6 +568,13 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
                      FrontierOut *fout = nullptr, int from_step = 0,
                      const int32_t *from_rows = nullptr, int64_t from_n = 0) {
   if (!g || (!out && !fout)) return fail(DM_ERR_ARG, "graph/out is NULL");
+  static const bool trace = std::getenv("DM_TRACE_HOST") != nullptr;  // debug: host phase times
+  auto t_start = std::chrono::steady_clock::now();
+  auto tr = [&](const char *what) {
+    if (!trace) return;
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_start).count();
+    std::fprintf(stderr, "[dm trace] %-18s %9.1f us\n", what, us);
+  };
   dm_match_opts opt;
   dm_match_opts_init(&opt);
   if (opt_in) opt = *opt_in;
@@ -491,8 +587,9 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   pstats.closure = g->closure;
   pstats.count_only = !(opt.output & DM_OUT_TABLE);
   pstats.max_degree = g->max_deg;
-  dm_status stt = build_plan(k, p_edges, pm, opt.motifs, opt.mode, plan, pstats);
+  dm_status stt = cached_plan(k, p_edges, pm, opt.motifs, opt.mode, pstats, plan);
   if (stt != DM_OK) return stt;
+  tr("plan");
   int64_t sb = std::max<int64_t>(0, opt.seed_begin);
   int64_t se = opt.seed_end < 0 ? g->n : std::min<int64_t>(opt.seed_end, g->n);
   if (se < sb) se = sb;
@@ -518,7 +615,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   c.mem_budget = opt.mem_budget;
   if (!c.mem_budget) {
     size_t fr = 0, tot = 0;
-    CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+    CK(cached_mem_info(g->device, &fr, &tot), "cudaMemGetInfo");
     // memory already cached by the stream-ordered pool is reusable too
     cudaMemPool_t pool;
     uint64_t reserved = 0, used = 0;
@@ -531,6 +628,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   }
   c.prof.on = (opt.flags & DM_MATCH_PROFILE) != 0;
   c.prof.s = c.s;
+  tr("setup+meminfo");
 
   const int nst = (int)plan.steps.size();
   if (stop_at >= 0 && (stop_at < 1 || stop_at >= nst))
@@ -563,8 +661,8 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   } ag{c};
   CK(cudaMemsetAsync(c.d_acc, 0, sizeof(unsigned long long) * nacc, c.s), "memset");
   if (c.prof.on) {
-    cudaEventCreate(&c.prof.t0);
-    cudaEventCreate(&c.prof.t1);
+    c.prof.t0 = event_pool().get();
+    c.prof.t1 = event_pool().get();
     cudaEventRecord(c.prof.t0, c.s);
   }
 
@@ -578,8 +676,10 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
       for (uint64_t i = 0; i < count; ++i) res->rows[i] = (int32_t)(sb + (int64_t)i);
     }
   } else {
+    tr("before steps");
     if (from_step > 0) stt = run_step(c, from_step, from_rows, from_n, 0);
     else stt = run_step(c, 0, nullptr, se - sb, sb);
+    tr("steps");
     if (stt != DM_OK) {
       if (c.d_front) cudaFreeAsync(c.d_front, c.s);
       return stt;
@@ -630,6 +730,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   }
   res->count = count;
   res->stats = c.st;
+  tr("done");
   rg.keep = true;
   *out = res;
   return DM_OK;
