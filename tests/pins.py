@@ -195,3 +195,34 @@ def brute_force(n, edges, k, p_edges, induced=False):
 
 def rows_to_tuples(rows):
     return [tuple(int(x) for x in r) for r in np.asarray(rows).tolist()]
+
+
+# ------------------------------------------------------------------ native full-scale pins
+def _pins_native():
+    """ctypes handle of tests/pins_native.c (built with gcc on first use; test infra only)."""
+    import ctypes
+    import os
+    import subprocess
+    here = os.path.dirname(os.path.abspath(__file__))
+    src = os.path.join(here, "pins_native.c")
+    lib = os.path.join(here, "libpins_native.so")
+    if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+        tmp = lib + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-pthread", src, "-o", tmp])
+        os.replace(tmp, lib)
+    L = ctypes.CDLL(lib)
+    for f in ("pins_triangles_labelled", "pins_diamonds_labelled", "pins_k4_distinct"):
+        fn = getattr(L, f)
+        fn.restype = ctypes.c_uint64
+        fn.argtypes = [ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int]
+    return L
+
+
+def native_counts(n, edges, which, threads=None):
+    """Exact labelled triangles / labelled diamonds / distinct K4 by sorted-list merges."""
+    import os
+    e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+    L = _pins_native()
+    fn = {"tri": L.pins_triangles_labelled, "diamond": L.pins_diamonds_labelled,
+          "k4": L.pins_k4_distinct}[which]
+    return int(fn(n, e.ctypes.data, e.shape[0], threads or os.cpu_count() or 1))

@@ -202,6 +202,18 @@ def test_config4_rmat16_counts(dm):
     assert G.match(*g.diamond()).count == diamonds_labelled(A)
 
 
+def test_config4_full_scale_diamond_k4(dm):
+    """Config 4 at full size in bench.py's launch configuration (R-MAT scale 20, ef 16, count
+    mode): labelled diamonds and 4-cliques against the native exact counters (P-dia via
+    per-edge sorted merges; P-K4 via a degree-oriented counter) -- the oracle would need ~1e5
+    core-seconds here."""
+    from pins import native_counts
+    n, e = g.rmat(20, 16, seed=1)
+    G = dm.Graph(n, e, drop_self_loops=True)
+    assert G.match(*g.diamond()).count == native_counts(n, e, "diamond")
+    assert G.match(*g.clique(4)).count == 24 * native_counts(n, e, "k4")
+
+
 def test_config4_rmat13_k4_count(dm):
     n, e = g.rmat(13, 16, seed=2)
     G = dm.Graph(n, e, drop_self_loops=True)

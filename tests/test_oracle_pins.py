@@ -202,6 +202,22 @@ def test_oracle_rmat_diamond_k4(scale):
         24 * k4_count_oriented(n, e)
 
 
+def test_native_pins_agree_with_closed_forms_and_oracle():
+    """The native full-scale counters (tests/pins_native.c) against tr(A^3), the diamond closed
+    form, and the oracle's K4 count, on R-MAT scale 11/12."""
+    from pins import native_counts
+    for scale in (11, 12):
+        n, e = g.rmat(scale, 16, seed=2)
+        A = simple_adj(n, e)
+        assert native_counts(n, e, "tri") == tri_labelled(A)
+        assert native_counts(n, e, "diamond") == diamonds_labelled(A)
+    n, e = g.rmat(11, 16, seed=2)
+    assert 24 * native_counts(n, e, "k4") == oracle.match(n, e, *g.clique(4), drop_self_loops=True,
+                                                          table=False).count
+    n, e = g.clique(7)
+    assert native_counts(n, e, "k4") == 35 and native_counts(n, e, "tri") == 210
+
+
 # ------------------------------------------------------------------------- metamorphic
 def test_oracle_relabel_equivariance():
     """P-meta: relabelling the data graph by sigma maps the result set by sigma."""
