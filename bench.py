@@ -290,20 +290,19 @@ def main():
     # ---------------- roofline of the dominant kernel (SURVEY §8(d) byte model)
     # Launch kinds: "single" = the fused join step of every materialized level (single pass:
     # join + filters + look-back prefix + write), "count" = the count-only last step.  Bytes per
-    # launch follow SURVEY §8(d): read rows 4*w*|F_i| (0 for the implicit seed) + key lookups
-    # 8*|F_i| + candidates 4*C_i + probes 4*Q_i (+ write 4*w_{i+1}*|F_{i+1}| for "single").
+    # launch follow SURVEY §8(d) with the stored id width e (4, or 2 for 16-bit levels): read
+    # rows e*w*|F_i| (0 for the implicit seed) + key lookups 8*|F_i| + candidates 4*C_i + probes
+    # 4*Q_i (+ write e*w_{i+1}*|F_{i+1}| for "single").
     kinds = {"join_single": [0.0, 0.0, 0], "join_count": [0.0, 0.0, 0]}
-    for s in stats:
+    for s in stats:  # per-step algorithmic bytes come from the library (dm_match_stats)
         for i in range(s["num_steps"]):
-            win = 0 if i == 0 else s["width_in"][i]
-            read = 4.0 * win * s["rows_in"][i] + 8.0 * s["rows_in"][i] + 4.0 * s["candidates"][i] + 4.0 * s["probes"][i]
             if s["ms_count"][i] > 0:
                 kinds["join_count"][0] += s["ms_count"][i]
-                kinds["join_count"][1] += read
+                kinds["join_count"][1] += s["bytes_model"][i]
                 kinds["join_count"][2] += 1
             if s["ms_write"][i] > 0:
                 kinds["join_single"][0] += s["ms_write"][i]
-                kinds["join_single"][1] += read + 4.0 * s["width_out"][i] * s["rows_out"][i]
+                kinds["join_single"][1] += s["bytes_model"][i]
                 kinds["join_single"][2] += 1
     dom = max(kinds, key=lambda kk: kinds[kk][0])
     ms, byts, launches = kinds[dom]

@@ -88,7 +88,7 @@ typedef struct {
   int32_t num_steps;             /* executed join steps (seed included)                    */
   int32_t num_launches;          /* kernels launched by this dm_match call                 */
   int32_t num_chunks;            /* frontier chunks processed (>= num_steps when chunked)  */
-  int32_t reserved;
+  int32_t elem_bytes;            /* bytes per stored vertex id in frontier levels (4 or 2)  */
   uint64_t rows_in[DM_MAX_STEPS];    /* |F_i| summed over chunks                           */
   uint64_t rows_out[DM_MAX_STEPS];   /* |F_{i+1}| (survivors)                              */
   uint64_t candidates[DM_MAX_STEPS]; /* C_i: join matches before filters (first new vertex,

@@ -57,7 +57,7 @@ class _Opts(ctypes.Structure):
 
 class _Stats(ctypes.Structure):
     _fields_ = [("num_steps", ctypes.c_int32), ("num_launches", ctypes.c_int32),
-                ("num_chunks", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("num_chunks", ctypes.c_int32), ("elem_bytes", ctypes.c_int32),
                 ("rows_in", ctypes.c_uint64 * DM_MAX_STEPS),
                 ("rows_out", ctypes.c_uint64 * DM_MAX_STEPS),
                 ("candidates", ctypes.c_uint64 * DM_MAX_STEPS),
@@ -231,6 +231,7 @@ def _stats_dict(s: _Stats) -> dict:
     n = s.num_steps
     return {
         "num_steps": n, "num_launches": s.num_launches, "num_chunks": s.num_chunks,
+        "elem_bytes": s.elem_bytes,
         "rows_in": list(s.rows_in)[:n], "rows_out": list(s.rows_out)[:n],
         "candidates": list(s.candidates)[:n], "probes": list(s.probes)[:n],
         "width_in": list(s.width_in)[:n], "width_out": list(s.width_out)[:n],

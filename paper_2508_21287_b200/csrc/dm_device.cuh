@@ -60,6 +60,12 @@ constexpr int kModeSingle = 2;
 // Frontier rows are stored with a 16-byte aligned stride: row_stride(w) int32 words, the
 // padding words hold -1 (never a vertex id).
 __host__ __device__ inline int row_stride(int w) { return (w + 3) & ~3; }
+// 16-bit storage (graphs with n <= 65535, count-only ELL plans): rows of round_up(w, 8) uint16
+// ids (16-byte rows, padding 0xFFFF = -1 when widened).  row_words = int32 words per stored row.
+__host__ __device__ inline int row_stride16(int w) { return (w + 7) & ~7; }
+__host__ __device__ inline int row_words(int w, int elem) {
+  return elem == 2 ? row_stride16(w) / 2 : row_stride(w);
+}
 
 // Device copy of one executed step (passed by value as a kernel parameter).
 struct DevStep {
@@ -88,6 +94,8 @@ struct StepIO {
   uint64_t cap;               // single pass: output capacity in rows
   int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
   const int32_t *ell;         // row-serial kernel: ELL adjacency (max degree <= 4) or nullptr
+  int32_t elem;               // bytes per stored vertex id in `in`: 4 (int32) or 2 (uint16)
+  int32_t out_elem;           // bytes per stored vertex id in `out`
 };
 
 size_t step_smem_bytes(int in_w, bool write_pass);

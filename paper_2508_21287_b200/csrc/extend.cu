@@ -162,6 +162,41 @@ __device__ __forceinline__ void load_tile(int32_t *rows, int ss, int ws, const S
     __syncthreads();
     return;
   }
+  if (io.elem == 2) {  // 16-bit rows: 16-byte loads of 8 ids, widened to int32 in shared memory
+    const int s16 = row_stride16(ws > 0 ? ws : 1);  // ws is row_stride(w); chunks of 8 ids
+    const int nq8 = s16 >> 3;
+    const uint4 *src16 = reinterpret_cast<const uint4 *>(
+        reinterpret_cast<const uint16_t *>(io.in) + (int64_t)r0 * s16);
+    const int total = nrows * nq8;  // chunks of the tile are contiguous in global memory
+    for (int i0 = 0; i0 < total; i0 += 4 * kStepThreads) {
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {  // issue all loads first (memory-level parallelism)
+        const int i = i0 + k * kStepThreads + tid;
+        v[k] = i < total ? __ldcs(src16 + i) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int i = i0 + k * kStepThreads + tid;
+        if (i >= total) break;
+        const int r = i / nq8, q = i - r * nq8;
+        const uint32_t u[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+        int32_t o[8];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const uint32_t lo = u[t] & 0xffffu, hi = u[t] >> 16;
+          o[2 * t] = lo == 0xffffu ? -1 : (int32_t)lo;
+          o[2 * t + 1] = hi == 0xffffu ? -1 : (int32_t)hi;
+        }
+        // chunk q covers ids [8q, 8q+8); smem rows hold ss >= ws int32 words (ws multiple of 4)
+        int32_t *d = rows + r * ss + 8 * q;
+        if (8 * q < ws) reinterpret_cast<int4 *>(d)[0] = make_int4(o[0], o[1], o[2], o[3]);
+        if (8 * q + 4 < ws) reinterpret_cast<int4 *>(d)[1] = make_int4(o[4], o[5], o[6], o[7]);
+      }
+    }
+    __syncthreads();
+    return;
+  }
   const int32_t *src = io.in + r0 * ws;
   if (ss == ws) {
     if (tid == 0) {
@@ -491,6 +526,54 @@ __device__ __forceinline__ void flush_rows(const int32_t *rows, const int32_t *s
       v.w = k1 == 3 ? x1 : v.w;
     }
     out4[(base + o) * nq + q] = v;
+  }
+}
+
+
+// 16-bit variant of the survivor flush: lanes -> (output row, 8-id chunk); each lane reads the
+// parent ids from the int32 smem row, patches the new vertices, packs to uint16 and stores 16 B.
+__device__ __forceinline__ int32_t pick8(const int4 &a, const int4 &b, int i) {
+  return i < 4 ? (i == 0 ? a.x : i == 1 ? a.y : i == 2 ? a.z : a.w)
+               : (i == 4 ? b.x : i == 5 ? b.y : i == 6 ? b.z : b.w);
+}
+
+__device__ __forceinline__ void flush_rows16(const int32_t *rows, const int32_t *sv_x,
+                                             const int32_t *map, int S, int w, int n_new,
+                                             int fill, int32_t *__restrict__ out, int64_t base) {
+  const int ws = row_stride(w), ss = smem_stride(w);
+  const int nq = row_stride16(w + n_new) >> 3;
+  int lpr = 1;
+  while (lpr < nq) lpr <<= 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = kStepThreads / 32;
+  const int q = lane & (lpr - 1), rpi = 32 / lpr, sub = lane / lpr;
+  if (q >= nq) return;
+  uint4 *out16 = reinterpret_cast<uint4 *>(out);
+  const int c0 = 8 * q;
+  const bool tail = c0 + 8 > w;  // chunk holds column w or w+1 (or padding)
+  for (int o = warp * rpi + sub; o < fill; o += nwarps * rpi) {
+    const int m = map[o];
+    const int r = m >> 4, sl = r * S + (m & 15);
+    const int32_t *prow = rows + r * ss;
+    const int4 neg = make_int4(-1, -1, -1, -1);
+    const int4 a = c0 < ws ? reinterpret_cast<const int4 *>(prow + c0)[0] : neg;
+    const int4 b = c0 + 4 < ws ? reinterpret_cast<const int4 *>(prow + c0 + 4)[0] : neg;
+    int32_t x0 = -1, x1 = -1;
+    if (tail) {
+      x0 = sv_x[2 * sl];
+      x1 = sv_x[2 * sl + 1];
+    }
+    uint32_t packed[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int32_t lo = pick8(a, b, 2 * t), hi = pick8(a, b, 2 * t + 1);
+      const int cl = c0 + 2 * t, ch = cl + 1;
+      if (tail) {
+        lo = cl == w ? x0 : ((cl == w + 1 && n_new == 2) ? x1 : (cl >= w ? -1 : lo));
+        hi = ch == w ? x0 : ((ch == w + 1 && n_new == 2) ? x1 : (ch >= w ? -1 : hi));
+      }
+      packed[t] = ((uint32_t)lo & 0xffffu) | ((uint32_t)hi << 16);
+    }
+    out16[(base + o) * nq + q] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
 }
 
@@ -856,7 +939,9 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
   const bool any_ovf = __syncthreads_or(ovf);
   if (!any_ovf)
     for (int i = 0; i < ns; ++i) map[pos + i] = (tid << 4) | i;
-  if (tid < 32) {
+  if (MODE == kModeWrite) {  // re-run at an exact offset (no look-back)
+    if (tid == 0) s_bc = io.block_off[tile] - io.out_base;
+  } else if (tid < 32) {
     const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
     if (tid == 0) {
       atomicAdd(io.ctrl + 2, (unsigned long long)agg);
@@ -868,12 +953,27 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
   __syncthreads();
   if (s_bc == ~0ull) return;
   if (!any_ovf) {
-    flush_rows(rows, nullptr, sv_x, map, S, w, st.n_new, agg, io.out, (int64_t)s_bc);
+    if (io.out_elem == 2) flush_rows16(rows, sv_x, map, S, w, st.n_new, agg, io.out, (int64_t)s_bc);
+    else flush_rows(rows, nullptr, sv_x, map, S, w, st.n_new, agg, io.out, (int64_t)s_bc);
     return;
   }
   // a row overflowed its slots: every thread re-enumerates its row and writes its survivors
   // directly at their final positions (same order, uncoalesced; rare)
-  if (tid < nrows && ns > 0) {
+  if (tid < nrows && ns > 0 && io.out_elem == 2) {
+    const int32_t *row = rows + tid * ss;
+    const int W = w + st.n_new, s16 = row_stride16(W);
+    uint16_t *dst = reinterpret_cast<uint16_t *>(io.out) + ((int64_t)s_bc + pos) * s16;
+    uint32_t dc = 0, dp = 0;
+    enumerate(
+        [&](int32_t x0, int32_t x1) {
+          for (int c = 0; c < s16; ++c) {
+            const int32_t v = c < w ? row[c] : (c == w ? x0 : ((c == w + 1 && st.n_new == 2) ? x1 : -1));
+            dst[c] = (uint16_t)(v & 0xffff);
+          }
+          dst += s16;
+        },
+        dc, dp);
+  } else if (tid < nrows && ns > 0) {
     const int32_t *row = rows + tid * ss;
     const int nq = row_stride(w + st.n_new) >> 2, nqs = ws >> 2, qw = w >> 2;
     int4 *dst = reinterpret_cast<int4 *>(io.out) + ((int64_t)s_bc + pos) * nq;
@@ -1178,7 +1278,7 @@ template <int MODE>
 cudaError_t launch(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t num_tiles,
                    cudaStream_t s) {
   if (num_tiles <= 0) return cudaSuccess;
-  if (MODE != kModeWrite && use_row_serial(st, g)) {
+  if ((MODE != kModeWrite || io.elem == 2 || io.out_elem == 2) && use_row_serial(st, g)) {
     StepIO io2 = io;
     io2.slots = row_slots(st, g);
     size_t smem = rows_smem_bytes(st.in_w, MODE != kModeCount, io2.slots);

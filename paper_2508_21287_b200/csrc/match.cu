@@ -176,12 +176,21 @@ struct Ctx {
   int32_t *d_res = nullptr;             // table mode: rows in column (match) order
   uint64_t res_rows = 0, res_cap = 0;
   std::vector<double> ratio;            // observed output/input rows per step (capacity estimate)
+  int elem = 4;                         // bytes per stored vertex id in frontier levels (4 or 2)
   int stop_at = -1;                     // dm_match_prefix: collect level `stop_at` instead of running it
   int32_t *d_front = nullptr;           //   collected rows (stride row_stride(w))
   uint64_t front_rows = 0, front_cap = 0;
   dm_match_stats st;
   Prof prof;
 };
+
+// Bytes per stored vertex id of frontier level `lvl` (the input of step lvl): 16-bit levels when
+// enabled, except the level read by a count-only last step (kept int32 so that kernel can
+// take its tile with one TMA bulk copy; it is compute-bound, not byte-bound).
+int level_elem(const Ctx &c, int lvl) {
+  if (c.elem == 4) return 4;
+  return (lvl == (int)c.plan->steps.size() - 1 && !c.table) ? 4 : 2;
+}
 
 dm_status cuda_fail(cudaError_t e, const char *what) {
   return fail(e == cudaErrorMemoryAllocation ? DM_ERR_OOM : DM_ERR_CUDA,
@@ -273,7 +282,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   const int nsteps = (int)c.plan->steps.size();
   const DevStep &D = c.dsteps[(size_t)si];
   const bool last = si == nsteps - 1;
-  const int W = row_stride(D.in_w + D.n_new);  // stored (16-byte padded) output row width
+  const int W = row_words(D.in_w + D.n_new, level_elem(c, si + 1));  // int32 words per stored row
   const int64_t tiles = (in_rows + kTileRows - 1) / kTileRows;
   c.st.rows_in[si] += (uint64_t)in_rows;
   c.st.num_chunks++;
@@ -283,6 +292,8 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   io.in_rows = in_rows;
   io.seed_base = seed_base;
   io.block_begin = 0;
+  io.elem = level_elem(c, si);
+  io.out_elem = level_elem(c, si + 1);
   io.stats = c.d_acc + kAccSlots + 2 * kAccSlots * si;
 
   if (last && !c.table) {  // count-only last step: reduce, never materialize
@@ -364,7 +375,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     }
     return run_step(c, si + 1, out, (int64_t)total, 0);
   }
-  c.st.reserved++;  // re-run count (tiles that did not fit)
+
   // ---- some tiles did not fit: exact tile prefix from the look-back status words
   DevBuf<uint64_t> excl;
   CK(excl.alloc((size_t)tiles + 1, c.s), "excl");
@@ -636,6 +647,9 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   if (from_step != 0 && (from_step < 1 || from_step >= nst || (from_n > 0 && !from_rows)))
     return fail(DM_ERR_ARG, "from_step must be in [1, num_steps) with device rows");
   c.stop_at = stop_at;
+  // 16-bit frontier storage: count-only plans on max-degree-4 graphs with 16-bit vertex ids
+  // (every step then runs in the row-serial kernels); not for tables or exchanged levels.
+  if (!c.table && stop_at < 0 && from_step == 0 && g->d_ell && g->n <= 65535) c.elem = 2;
   dm_result *res = new (std::nothrow) dm_result;
   if (!res) return fail(DM_ERR_OOM, "host allocation failed");
   res->k = k;
@@ -724,11 +738,13 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     c.st.probes[i] = slot_sum(2 * kAccSlots + 2 * kAccSlots * i);
     const bool lastc = (i + 1 == plan.steps.size()) && !c.table;
     const double win = (i == 0) ? 0.0 : (double)c.st.width_in[i];  // the seed input is implicit
-    c.st.bytes_model[i] = 4.0 * win * (double)c.st.rows_in[i] + 8.0 * (double)c.st.rows_in[i] +
+    const double ebi = (double)level_elem(c, (int)i), ebo = (double)level_elem(c, (int)i + 1);
+    c.st.bytes_model[i] = ebi * win * (double)c.st.rows_in[i] + 8.0 * (double)c.st.rows_in[i] +
                           4.0 * (double)c.st.candidates[i] + 4.0 * (double)c.st.probes[i] +
-                          (lastc ? 0.0 : 4.0 * c.st.width_out[i] * (double)c.st.rows_out[i]);
+                          (lastc ? 0.0 : ebo * c.st.width_out[i] * (double)c.st.rows_out[i]);
   }
   res->count = count;
+  c.st.elem_bytes = c.elem;  // bytes per stored vertex id in the frontier levels
   res->stats = c.st;
   tr("done");
   rg.keep = true;
