@@ -15,7 +15,7 @@ for (i, k), m in per.items():
     t = m.get("gpu__time_duration.sum", 0.0)
     tot_t += t
     mk = re.search(r"k_(?:rows|step)<(\d)", k)
-    if "k_pairs" in k:
+    if "k_pairs" in k or "k_deep" in k:
         kind = "join_count"
     elif mk:
         kind = {"0": "join_count", "1": "join_rerun", "2": "join_single"}[mk.group(1)]
