@@ -9,11 +9,11 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdeltamotif.so")
-SOURCES = ["errors.cpp", "planner.cpp", "graph.cu", "extend.cu", "match.cu"]
+SOURCES = ["errors.cpp", "planner.cpp", "graph.cu", "extend.cu", "tail.cu", "pairs.cu", "match.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
-         "-shared", "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
 def _stale() -> bool:
@@ -28,10 +28,28 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
-    if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    headers.append(os.path.join(ROOT, "include", "deltamotif.h"))
+    newest_hdr = max(os.path.getmtime(h) for h in headers)
+    objs, procs = [], []
+    for src in SOURCES:  # one nvcc per translation unit, in parallel; stale objects only
+        obj = os.path.join(objdir, src + ".o")
+        objs.append(obj)
+        spath = os.path.join(CSRC, src)
+        if (not force and os.path.exists(obj)
+                and os.path.getmtime(obj) > max(os.path.getmtime(spath), newest_hdr)):
+            continue
+        cmd = [NVCC, *ARCH, *FLAGS, "-c", spath, "-o", obj + ".tmp"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        procs.append((subprocess.Popen(cmd), obj))
+    for p, obj in procs:
+        if p.wait() != 0:
+            raise subprocess.CalledProcessError(p.returncode, "nvcc")
+        os.replace(obj + ".tmp", obj)
+    subprocess.check_call([NVCC, *ARCH, "-shared", *objs, "-o", tmp])
     os.replace(tmp, LIB)
     return LIB
 

@@ -109,6 +109,9 @@ int pair_mode_of(const DevStep &st);
 bool row_serial_step(const DevStep &st, const dm_graph &g);
 cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g, int pair_mode,
                          cudaStream_t s);
+// deep count-only last step (3..kMaxNew new vertices) on ELL graphs (tail.cu: k_deep)
+cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
+                        cudaStream_t s);
 cudaError_t launch_status_to_excl(const unsigned long long *status, int64_t tiles, uint64_t *excl,
                                   cudaStream_t s);
 

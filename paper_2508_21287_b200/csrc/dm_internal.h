@@ -38,7 +38,7 @@ struct StepVertex {
 };
 
 // One executed join step: 1 or 2 new vertices (up to kMaxNew for a count-only last step on a
-// max-degree-4 graph, where the row-serial kernel enumerates them depth-first).
+// max-degree-4 graph, where the tail kernel enumerates them without materializing the levels).
 constexpr int kMaxNew = 4;
 struct Step {
   int slice = -1;

@@ -186,7 +186,8 @@ struct Ctx {
 
 // Bytes per stored vertex id of frontier level `lvl` (the input of step lvl): 16-bit levels when
 // enabled, except the level read by a count-only last step (kept int32 so that kernel can
-// take its tile with one TMA bulk copy; it is compute-bound, not byte-bound).
+// take its tile with one TMA bulk copy; it is compute-bound, not byte-bound: measured on
+// config 5, a 16-bit input level saved 0.1 ms in the producer and cost 1.2 ms in the tail).
 int level_elem(const Ctx &c, int lvl) {
   if (c.elem == 4) return 4;
   return (lvl == (int)c.plan->steps.size() - 1 && !c.table) ? 4 : 2;

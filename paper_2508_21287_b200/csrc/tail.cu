@@ -1,0 +1,151 @@
+// tail.cu -- the deep count-only last step ("tail", 3-4 new vertices) of a join program on
+// ELL graphs (max degree <= 4): the last joins of the program are executed per frontier row
+// without materializing their levels -- the larger-motif joins of PAPER.md §3.5
+// applied row by row.  Every candidate is still inspected: the all-distinct rule (P:237,
+// S:213), the closing-edge probes of multi-key joins (Fig. 2 C1/C2) and, in induced
+// mode, the non-edge probes.  CTA = tile of 256 rows in shared memory; thread = row; the
+// recursion is unrolled at compile time (static indices into the assigned new vertices).
+//
+// Measured alternatives (config 5, P30 on heavy-hex w=31, B200, r01): deeper tails (5-8 new
+// vertices, which would skip materializing the last levels) lose -- a warp-cooperative
+// breadth-first tail in shared memory ran 12.2 ms, an iterative lockstep per-thread DFS with
+// row stealing 11.7 ms and an unrolled 8-deep recursion 24 ms, against 5.4 ms for this 4-deep
+// tail plus 4.7 ms for materializing the two extra levels; see DESIGN.md §5.
+#include "extend_common.cuh"
+
+namespace dm {
+namespace {
+
+// ---- depth-first enumeration of a 3-4 vertex count-only last step (ELL graphs): the larger
+// motif joins of PAPER.md §3.5 executed per row without materializing the levels
+__device__ __forceinline__ int32_t colval4(const int32_t *row, int w, int c, const int32_t (&x)[kMaxNew]) {
+  const int k = c - w;
+  return k < 0 ? row[c] : (k == 0 ? x[0] : (k == 1 ? x[1] : (k == 2 ? x[2] : x[3])));
+}
+
+template <int J, int NQ>
+__device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *row, int w, int ws,
+                                            unsigned long long bloom, int32_t (&x)[kMaxNew],
+                                            const int4 *__restrict__ ell, uint32_t &cand,
+                                            uint32_t &probes) {
+  if constexpr (J >= kMaxNew) {
+    return 1u;
+  } else {
+    if (J >= st.n_new) return 1u;
+    int best = st.nbr[J][0];
+    int4 nb = ell_row(ell, colval4(row, w, best, x));
+    const bool extra = st.n_nbr[J] > 1 || st.n_non[J] > 0;
+    if (st.n_nbr[J] > 1) {
+      int bd = ell_deg(nb);
+      for (int t = 1; t < st.n_nbr[J]; ++t) {
+        const int c = st.nbr[J][t];
+        const int4 e = ell_row(ell, colval4(row, w, c, x));
+        const int d = ell_deg(e);
+        if (d < bd) {
+          bd = d;
+          nb = e;
+          best = c;
+        }
+      }
+    }
+    unsigned tot = 0;
+#pragma unroll 1
+    for (int i = 0; i < 4; ++i) {
+      const int32_t y = nb.x;  // candidates in ascending order: shift the int4 down
+      nb.x = nb.y;
+      nb.y = nb.z;
+      nb.z = nb.w;
+      nb.w = -1;
+      if (y < 0) break;
+      ++cand;
+      bool ok = true;
+#pragma unroll
+      for (int t = 0; t < J; ++t) ok &= x[t] != y;  // distinct from the other new vertices
+      if (!ok) continue;
+      if ((bloom & bloom_bit(y)) && in_row_q<NQ>(row, ws, y)) continue;  // ... and from the row
+      if (extra) {
+        for (int t = 0; t < st.n_nbr[J] && ok; ++t) {
+          const int c = st.nbr[J][t];
+          if (c == best) continue;
+          ++probes;
+          ok = ell_has(ell, colval4(row, w, c, x), y);
+        }
+        for (int t = 0; t < st.n_non[J] && ok; ++t) {
+          ++probes;
+          ok = !ell_has(ell, colval4(row, w, st.non[J][t], x), y);
+        }
+        if (!ok) continue;
+      }
+      x[J] = y;
+      tot += dfs_ell<J + 1, NQ>(st, row, w, ws, bloom, x, ell, cand, probes);
+    }
+    return tot;
+  }
+}
+
+// Deep count-only last step (3-4 new vertices, ELL graphs): tile -> smem, one thread per row,
+// depth-first enumeration (dfs_ell), CTA-reduced counters.
+template <int NQ>
+__global__ void __launch_bounds__(kStepThreads)
+    k_deep(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+           const int32_t *__restrict__ adj) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t s_bar;
+  const int w = st.in_w, ws = row_stride(w), ss = smem_stride(w);
+  const int tid = threadIdx.x;
+  const int64_t tile = io.block_begin + blockIdx.x;
+  const int64_t r0 = tile * kTileRows;
+  if (r0 >= io.in_rows) return;
+  const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
+  int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
+  load_tile(rows, ss, ws, io, r0, nrows, &s_bar);
+  uint32_t my_cand = 0, my_probe = 0;
+  unsigned ns = 0;
+  if (tid < nrows) {
+    int32_t x[kMaxNew] = {-1, -1, -1, -1};
+    const int32_t *row = rows + tid * ss;
+    unsigned long long bloom = 0;
+    for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
+    ns = dfs_ell<0, NQ>(st, row, w, ws, bloom, x, reinterpret_cast<const int4 *>(io.ell), my_cand,
+                        my_probe);
+  }
+  unsigned long long v3[3] = {my_cand, my_probe, ns};
+  block_sum3(v3);
+  if (tid == 0) {
+    const int slot = (int)(tile & (kAccSlots - 1));
+    if (io.stats) {
+      atomicAdd(io.stats + slot, v3[0]);
+      atomicAdd(io.stats + kAccSlots + slot, v3[1]);
+    }
+    if (io.block_cnt) io.block_cnt[tile] = v3[2];
+    if (io.total && v3[2]) atomicAdd(io.total + slot, v3[2]);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
+                        cudaStream_t s) {
+  if (io.in_rows <= 0 || tiles <= 0) return cudaSuccess;
+  StepIO io2 = io;
+  io2.ell = g.d_ell;
+  const size_t smem = sizeof(int32_t) * (size_t)kTileRows * smem_stride(st.in_w);
+  auto kern = k_deep<0>;
+  switch (row_stride(st.in_w) >> 2) {
+    case 1: kern = k_deep<1>; break;
+    case 2: kern = k_deep<2>; break;
+    case 3: kern = k_deep<3>; break;
+    case 4: kern = k_deep<4>; break;
+    case 5: kern = k_deep<5>; break;
+    case 6: kern = k_deep<6>; break;
+    case 7: kern = k_deep<7>; break;
+    case 8: kern = k_deep<8>; break;
+    default: break;
+  }
+  cudaError_t e = prep((const void *)kern, 0, smem);
+  if (e != cudaSuccess) return e;
+  kern<<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);
+  return cudaGetLastError();
+}
+
+}  // namespace dm

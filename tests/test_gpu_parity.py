@@ -253,6 +253,38 @@ def test_heavy_hex_count_mode_deep_steps(dm, w):
             assert r.count == o.count, (k, pe.tolist(), mode)
 
 
+@pytest.mark.parametrize("graph", ["grid120", "hh31"])
+def test_deep_tail_counts(dm, graph):
+    """Count mode with a deep tail (3-4 new vertices enumerated per row, never materialized) on
+    large max-degree-3/4 lattices (several tiles per level, 16-bit frontier levels): paths,
+    rings (closing edge into the materialized columns), trees, stars and random subgraphs
+    (several keys per vertex, known-duplicate shortcut only on the first key), both modes;
+    counts must equal the oracle's."""
+    if graph == "grid120":
+        n, e = g.grid(120)
+        pats = [g.path(9), g.ring(10), g.ring(8), g.star(4)]
+        sizes = (9, 10)
+    else:
+        n, e = g.ibm_heavy_hex(31)
+        pats = [g.path(12), g.path(14), g.ring(12), g.star(3)]
+        sizes = (12, 14)
+    G = dm.Graph(n, e)
+    for s in (1, 2):
+        pats.append(g.random_tree(sizes[0], s, max_degree=3) if graph == "grid120"
+                    else g.device_subtree(n, e, sizes[0], s))
+        k, pe, _ = g.random_connected_subgraph(n, e, sizes[1], s)
+        pats.append((k, pe))
+    deep = 0
+    for (k, pe) in pats:
+        for mode in ("mono", "induced"):
+            r = G.match(k, pe, mode=mode, profile=True)
+            st = r.stats
+            deep += (st["width_out"][-1] - st["width_in"][-1]) >= 3
+            o = oracle.match(n, e, k, pe, induced=(mode == "induced"), table=False)
+            assert r.count == o.count, (graph, k, pe.tolist(), mode)
+    assert deep >= 4
+
+
 def test_config5_random_subgraphs(dm):
     n, e = g.ibm_heavy_hex(31)
     G = dm.Graph(n, e)
