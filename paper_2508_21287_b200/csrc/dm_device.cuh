@@ -88,9 +88,10 @@ struct StepIO {
   uint64_t *block_cnt;        // count pass: survivors per tile (nullptr -> only total)
   unsigned long long *total;  // count pass: [tile % kAccSlots] += survivors (nullptr -> skip)
   unsigned long long *stats;  // [slot] += candidates, [kAccSlots + slot] += probes (or nullptr)
-  unsigned long long *status; // single pass: look-back status word per tile (zeroed)
-  unsigned long long *ctrl;   // single pass: [0] tile counter, [1] max(#tiles - unwritten tile),
-                              //   [2] += survivors (all zero-initialised)
+  unsigned long long *status; // single pass (k_step): look-back status word per tile (zeroed)
+  unsigned long long *agg;    // single pass: survivors per tile ([tiles] = 0; exact re-run prefix)
+  unsigned long long *ctrl;   // single pass: [0] tile counter, [1] max(#tiles - first tile that
+                              //   must be re-run), [2] += survivors / output reservation (zeroed)
   uint64_t cap;               // single pass: output capacity in rows
   int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
   const int32_t *ell;         // row-serial kernel: ELL adjacency (max degree <= 4) or nullptr
@@ -112,8 +113,9 @@ cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g,
 // deep count-only last step (3..kMaxNew new vertices) on ELL graphs (tail.cu: k_deep)
 cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
                         cudaStream_t s);
-cudaError_t launch_status_to_excl(const unsigned long long *status, int64_t tiles, uint64_t *excl,
-                                  cudaStream_t s);
+// excl[t] = sum of agg[0..t) for t in [0, tiles] (agg[tiles] must be 0)
+cudaError_t launch_agg_to_excl(const unsigned long long *agg, int64_t tiles, uint64_t *excl,
+                               cudaStream_t s);
 
 DevStep make_dev_step(const Step &st);
 

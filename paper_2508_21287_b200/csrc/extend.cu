@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(kStepThreads)
   if (tid < 32) {
     const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
     if (tid == 0) {
+      io.agg[tile] = (unsigned long long)agg;
       atomicAdd(io.ctrl + 2, (unsigned long long)agg);
       const bool fits = !ovf && excl + (unsigned long long)agg <= io.cap;
       if (!fits) atomicMax(io.ctrl + 1, (unsigned long long)(ntiles_of(io) - tile));
@@ -556,16 +557,19 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
   const bool any_ovf = __syncthreads_or(ovf);
   if (!any_ovf)
     for (int i = 0; i < ns; ++i) map[pos + i] = (tid << 4) | i;
-  if (MODE == kModeWrite) {  // re-run at an exact offset (no look-back)
+  if (MODE == kModeWrite) {  // re-run at an exact offset
     if (tid == 0) s_bc = io.block_off[tile] - io.out_base;
-  } else if (tid < 32) {
-    const unsigned long long excl = lookback(io.status, tile, (unsigned long long)agg);
-    if (tid == 0) {
-      atomicAdd(io.ctrl + 2, (unsigned long long)agg);
-      const bool fits = excl + (unsigned long long)agg <= io.cap;
-      if (!fits) atomicMax(io.ctrl + 1, (unsigned long long)(ntiles_of(io) - tile));
-      s_bc = fits ? excl : ~0ull;
-    }
+  } else if (tid == 0) {
+    // output space by atomic reservation: no tile waits for its predecessors (a decoupled
+    // look-back here stalled the CTA at the barrier for ~25% of the step).  The rows of a level
+    // are then in tile-completion order; counts do not depend on it and tables are sorted at
+    // the end (a9).  A tile that does not fit makes the host re-run the whole step at exact
+    // offsets (kModeWrite, tile order) from the per-tile counts.
+    io.agg[tile] = (unsigned long long)agg;
+    const unsigned long long base = agg ? atomicAdd(io.ctrl + 2, (unsigned long long)agg) : 0ull;
+    const bool fits = base + (unsigned long long)agg <= io.cap;
+    if (!fits) atomicMax(io.ctrl + 1, (unsigned long long)ntiles_of(io));
+    s_bc = fits ? base : ~0ull;
   }
   __syncthreads();
   if (s_bc == ~0ull) return;
@@ -629,14 +633,6 @@ int row_slots(const DevStep &st, const dm_graph &g) {
   int64_t d = g.max_deg < 1 ? 1 : g.max_deg;
   int64_t s = st.n_new == 1 ? d : d * d;
   return (int)(s < kRowSlotsMax ? s : kRowSlotsMax);
-}
-
-// exclusive prefix over tiles from the look-back status words: excl[t] = inclusive[t-1]
-__global__ void k_status_to_excl(const unsigned long long *__restrict__ status, int64_t tiles,
-                                 uint64_t *__restrict__ excl) {
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= tiles;
-       t += (int64_t)gridDim.x * blockDim.x)
-    excl[t] = t == 0 ? 0 : (status[t - 1] & kValueMask);
 }
 
 template <int MODE, int NQ>
@@ -718,13 +714,19 @@ cudaError_t launch_step_single(const DevStep &st, const StepIO &io, const dm_gra
   return launch<kModeSingle>(st, io, g, num_tiles, s);
 }
 
-cudaError_t launch_status_to_excl(const unsigned long long *status, int64_t tiles, uint64_t *excl,
-                                  cudaStream_t s) {
-  int64_t b = (tiles + 1 + 255) / 256;
-  if (b < 1) b = 1;
-  if (b > 2048) b = 2048;
-  k_status_to_excl<<<(unsigned)b, 256, 0, s>>>(status, tiles, excl);
-  return cudaGetLastError();
+cudaError_t launch_agg_to_excl(const unsigned long long *agg, int64_t tiles, uint64_t *excl,
+                               cudaStream_t s) {
+  const unsigned long long *in = agg;
+  unsigned long long *out = reinterpret_cast<unsigned long long *>(excl);
+  size_t tmp_bytes = 0;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, in, out, (int64_t)(tiles + 1), s);
+  if (e != cudaSuccess) return e;
+  void *tmp = nullptr;
+  e = cudaMallocAsync(&tmp, tmp_bytes, s);
+  if (e != cudaSuccess) return e;
+  e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, (int64_t)(tiles + 1), s);
+  cudaFreeAsync(tmp, s);
+  return e;
 }
 
 DevStep make_dev_step(const Step &st) {

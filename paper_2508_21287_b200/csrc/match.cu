@@ -343,12 +343,16 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     live.add(cap * row_bytes);
     out = outb.p;
   }
-  DevBuf<unsigned long long> status, ctrl;
+  DevBuf<unsigned long long> status, ctrl, agg;
   CK(status.alloc((size_t)tiles, c.s), "status");
+  CK(agg.alloc((size_t)tiles + 1, c.s), "agg");
   CK(ctrl.alloc(3, c.s), "ctrl");
-  CK(cudaMemsetAsync(status.p, 0, sizeof(unsigned long long) * (size_t)tiles, c.s), "memset");
+  if (!row_serial_step(D, *c.g))  // look-back status words (candidate-partitioned kernel)
+    CK(cudaMemsetAsync(status.p, 0, sizeof(unsigned long long) * (size_t)tiles, c.s), "memset");
+  CK(cudaMemsetAsync(agg.p + tiles, 0, sizeof(unsigned long long), c.s), "memset");
   CK(cudaMemsetAsync(ctrl.p, 0, 3 * sizeof(unsigned long long), c.s), "memset");
   unsigned long long *hctrl = pinned_scratch();
+  io.agg = agg.p;
   io.status = status.p;
   io.ctrl = ctrl.p;
   io.cap = cap;
@@ -377,10 +381,10 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     return run_step(c, si + 1, out, (int64_t)total, 0);
   }
 
-  // ---- some tiles did not fit: exact tile prefix from the look-back status words
+  // ---- some tiles did not fit: exact tile prefix from the per-tile survivor counts
   DevBuf<uint64_t> excl;
   CK(excl.alloc((size_t)tiles + 1, c.s), "excl");
-  CK(launch_status_to_excl(status.p, tiles, excl.p, c.s), "status->excl");
+  CK(launch_agg_to_excl(agg.p, tiles, excl.p, c.s), "agg->excl");
   uint64_t written = 0;  // rows [0, written) are complete in `out`
   CK(cudaMemcpyAsync(&written, excl.p + tstar, sizeof(uint64_t), cudaMemcpyDeviceToHost, c.s), "D2H");
   CK(cudaStreamSynchronize(c.s), "sync");
