@@ -325,7 +325,9 @@ __host__ __device__ inline long long ntiles_of(const StepIO &io) {
 
 // Raise the dynamic shared-memory limit (and prefer the maximum carveout) of a kernel once per
 // (device, kernel) growth.  `which` is unused (kept for call-site readability).
-cudaError_t prep(const void *fn, int which, size_t smem) {
+// carveout: preferred shared-memory share of the unified L1/shared array in percent (100 = as
+// much shared memory as possible; lower leaves the rest to L1).
+cudaError_t prep(const void *fn, int which, size_t smem, int carveout = 100) {
   (void)which;
   static std::mutex mu;
   static std::map<std::pair<int, const void *>, size_t> configured;
@@ -337,7 +339,7 @@ cudaError_t prep(const void *fn, int which, size_t smem) {
   auto it = configured.find(key);
   if (it != configured.end() && it->second >= smem) return cudaSuccess;
   e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
   if (e == cudaSuccess) configured[key] = smem;
   return e;
 }

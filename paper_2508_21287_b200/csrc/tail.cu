@@ -11,6 +11,8 @@
 // breadth-first tail in shared memory ran 12.2 ms, an iterative lockstep per-thread DFS with
 // row stealing 11.7 ms and an unrolled 8-deep recursion 24 ms, against 5.4 ms for this 4-deep
 // tail plus 4.7 ms for materializing the two extra levels; see DESIGN.md §5.
+#include <cmath>
+
 #include "extend_common.cuh"
 
 namespace dm {
@@ -142,8 +144,29 @@ cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, 
     case 8: kern = k_deep<8>; break;
     default: break;
   }
-  cudaError_t e = prep((const void *)kern, 0, smem);
-  if (e != cudaSuccess) return e;
+  // Shared memory only for the register-limited number of resident CTAs; the rest of the
+  // unified array stays L1 for the ELL lists (160 KB on heavy-hex w=31): with the maximal
+  // carveout the ELL loads hit L1 70% of the time, the tile rows need only ~120 KB per SM.
+  static std::mutex mu;
+  static std::map<const void *, int> carve;
+  int cv = 100;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = carve.find((const void *)kern);
+    if (it == carve.end()) {
+      cudaError_t e = prep((const void *)kern, 0, smem);
+      if (e != cudaSuccess) return e;
+      int nb = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kStepThreads, smem);
+      if (e != cudaSuccess) return e;
+      const double need = (double)nb * (double)(smem + 1024);
+      cv = (int)std::ceil(100.0 * need / (228.0 * 1024.0));
+      cv = cv < 1 ? 1 : (cv > 100 ? 100 : cv);
+      e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributePreferredSharedMemoryCarveout, cv);
+      if (e != cudaSuccess) return e;
+      carve[(const void *)kern] = cv;
+    }
+  }
   kern<<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);
   return cudaGetLastError();
 }
