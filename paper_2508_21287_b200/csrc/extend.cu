@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
   };
   if (tid < nrows) enumerate(record, my_cand, my_probe);
   // statistics and count-mode totals: CTA reduction, one atomic per CTA on slot tile % 64
-  if (io.stats || MODE == kModeCount) {
+  auto reduce_stats = [&]() {
     unsigned long long v3[3] = {my_cand, my_probe, (unsigned long long)ns};
     block_sum3(v3);
     if (tid == 0) {
@@ -550,23 +550,29 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
         if (io.total && v3[2]) atomicAdd(io.total + slot, v3[2]);
       }
     }
+  };
+  if (MODE == kModeCount) {
+    reduce_stats();
+    return;
   }
-  if (MODE == kModeCount) return;
   int pos, agg;
   ScanI(tmp).ExclusiveSum(ns, pos, agg);
+  // Output space by atomic reservation: no tile waits for its predecessors (a decoupled
+  // look-back here stalled the CTA at the barrier for ~25% of the step).  The rows of a level
+  // are then in tile-completion order; counts do not depend on it and tables are sorted at the
+  // end (a9).  A tile that does not fit makes the host re-run the whole step at exact offsets
+  // (kModeWrite, tile order) from the per-tile counts.  The reservation is issued as soon as
+  // the tile total is known; its round trip overlaps the statistics reduction and the map.
+  unsigned long long base = 0;
+  if (MODE == kModeSingle && tid == 0 && agg) base = atomicAdd(io.ctrl + 2, (unsigned long long)agg);
+  if (io.stats) reduce_stats();
   const bool any_ovf = __syncthreads_or(ovf);
   if (!any_ovf)
     for (int i = 0; i < ns; ++i) map[pos + i] = (tid << 4) | i;
   if (MODE == kModeWrite) {  // re-run at an exact offset
     if (tid == 0) s_bc = io.block_off[tile] - io.out_base;
   } else if (tid == 0) {
-    // output space by atomic reservation: no tile waits for its predecessors (a decoupled
-    // look-back here stalled the CTA at the barrier for ~25% of the step).  The rows of a level
-    // are then in tile-completion order; counts do not depend on it and tables are sorted at
-    // the end (a9).  A tile that does not fit makes the host re-run the whole step at exact
-    // offsets (kModeWrite, tile order) from the per-tile counts.
     io.agg[tile] = (unsigned long long)agg;
-    const unsigned long long base = agg ? atomicAdd(io.ctrl + 2, (unsigned long long)agg) : 0ull;
     const bool fits = base + (unsigned long long)agg <= io.cap;
     if (!fits) atomicMax(io.ctrl + 1, (unsigned long long)ntiles_of(io));
     s_bc = fits ? base : ~0ull;
