@@ -40,7 +40,7 @@ extern "C" {
 #define DM_API
 #endif
 
-#define DM_ABI_VERSION 1
+#define DM_ABI_VERSION 2
 #define DM_MAX_PATTERN 64 /* max pattern vertices k */
 
 typedef struct dm_graph dm_graph;   /* device CSR of G_d (Res(M2), both orientations) */
@@ -101,6 +101,10 @@ typedef struct {
   double ms_write[DM_MAX_STEPS];     /* device ms in write-pass kernels of step i          */
   double ms_other;                   /* scans, canonical sort, copies                      */
   double ms_total;                   /* device ms from first to last launch                */
+  int32_t pipelined;                 /* 1: every step was enqueued without an intermediate host
+                                        synchronisation (repeated count query whose level
+                                        capacities came from the previous identical run)    */
+  int32_t reserved;
 } dm_match_stats;
 
 /* Fill *opt with defaults (DM_MONO, DM_OUT_COUNT, all motifs, whole graph, NULL stream). */

@@ -32,7 +32,7 @@ DM_GRAPH_DROP_SELF_LOOPS = 1
 DM_MATCH_PROFILE = 1
 DM_MAX_PATTERN = 64
 DM_MAX_STEPS = 64
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 MOTIF_SETS = {
     "all": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O,
@@ -67,7 +67,8 @@ class _Stats(ctypes.Structure):
                 ("bytes_model", ctypes.c_double * DM_MAX_STEPS),
                 ("ms_count", ctypes.c_double * DM_MAX_STEPS),
                 ("ms_write", ctypes.c_double * DM_MAX_STEPS),
-                ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double)]
+                ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double),
+                ("pipelined", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 _lib = None
@@ -237,6 +238,7 @@ def _stats_dict(s: _Stats) -> dict:
         "width_in": list(s.width_in)[:n], "width_out": list(s.width_out)[:n],
         "bytes_model": list(s.bytes_model)[:n], "ms_count": list(s.ms_count)[:n],
         "ms_write": list(s.ms_write)[:n], "ms_other": s.ms_other, "ms_total": s.ms_total,
+        "pipelined": bool(s.pipelined),
     }
 
 

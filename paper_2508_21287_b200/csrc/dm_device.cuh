@@ -19,6 +19,7 @@ struct dm_graph {
   int32_t *d_ell = nullptr;  // max degree <= 4: [n][4] adjacency (ELL, sorted, -1 padded)
   double sum_d2 = 0.0;       // sum of squared degrees (size-biased degree = sum_d2 / arcs)
   double closure = 0.0;      // sampled P[c in N(a) | a-b-c wedge] (triangle closure)
+  uint64_t gen = 0;          // process-unique creation id (keys host-side caches)
 };
 
 namespace dm {
@@ -93,6 +94,8 @@ struct StepIO {
   unsigned long long *ctrl;   // single pass: [0] tile counter, [1] max(#tiles - first tile that
                               //   must be re-run), [2] += survivors / output reservation (zeroed)
   uint64_t cap;               // single pass: output capacity in rows
+  const unsigned long long *d_in_rows;  // if set: the input row count, written on the device by
+                                        // the previous step (in_rows is then only an upper bound)
   int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
   const int32_t *ell;         // row-serial kernel: ELL adjacency (max degree <= 4) or nullptr
   int32_t elem;               // bytes per stored vertex id in `in`: 4 (int32) or 2 (uint16)

@@ -234,8 +234,10 @@ __device__ unsigned long long lookback(unsigned long long *status, int64_t tile,
 
 template <int MODE>
 __global__ void __launch_bounds__(kStepThreads)
-    k_step(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+    k_step(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
+  StepIO io = io_;  // device-written input size (sync-free chaining)
+  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typedef cub::BlockScan<long long, kStepThreads> ScanLL;
   typedef cub::BlockScan<int, kStepThreads> ScanI;
@@ -433,8 +435,10 @@ __global__ void __launch_bounds__(kStepThreads)
 // kernel (kModeWrite).  Output order is identical to k_step (row, then candidate order).
 template <int MODE, int NQ, bool ELL>
 __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ? 64 : 48)
-    k_rows(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+    k_rows(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
+  StepIO io = io_;  // device-written input size (sync-free chaining)
+  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typedef cub::BlockScan<int, kStepThreads> ScanI;
   __shared__ typename ScanI::TempStorage tmp;

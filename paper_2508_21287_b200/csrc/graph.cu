@@ -5,6 +5,7 @@
 //   orientations as 64-bit keys (u << 32 | v)) -> CUB radix sort -> CUB unique -> k_bounds
 //   (CSR offsets from the sorted keys, no atomics) + k_split (adjacency ids) -> max degree.
 // Every adjacency list comes out sorted ascending (the probe kernels binary-search it).
+#include <atomic>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -141,6 +142,8 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   } sg{s};
 
   dm_graph *g = new (std::nothrow) dm_graph;
+  static std::atomic<uint64_t> next_gen{1};
+  if (g) g->gen = next_gen.fetch_add(1);
   if (!g) return fail(DM_ERR_OOM, "host allocation failed");
   g->device = device;
   g->n = n;

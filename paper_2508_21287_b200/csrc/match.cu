@@ -137,6 +137,13 @@ struct Prof {
     cudaEventRecord(e.b, s);
     evs.push_back(e);
   }
+  void reset() {  // drop the per-step events of an abandoned attempt (keeps t0)
+    for (auto &e : evs) {
+      event_pool().put(e.a);
+      event_pool().put(e.b);
+    }
+    evs.clear();
+  }
   void finish(dm_match_stats &st) {
     if (!on) return;
     cudaStreamSynchronize(s);
@@ -445,6 +452,129 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   return DM_OK;
 }
 
+// ---------------------------------------------------------------------------------------
+// Sync-free count-mode pipeline.  The path above reads every level's size back to the host
+// (one stream synchronisation per step) to size the next buffer.  For a repeated query (the
+// same graph, pattern and seed range -- the bench loop, the paper's GPU* use) the growth
+// ratios of the previous run give the capacities up front: every step is enqueued at once,
+// each kernel reads its input size from the counter the previous kernel wrote on the device
+// (StepIO::d_in_rows; grids are sized for the capacity, surplus CTAs exit), and the host waits
+// once.  A level that would exceed its capacity is reported by its kernel (ctrl[1]); the
+// match is then re-run on the synchronising path (results never depend on the path).
+struct RatioCache {
+  std::mutex mu;
+  std::map<std::string, std::vector<double>> m;
+};
+RatioCache &ratio_cache() {
+  static RatioCache rc;
+  return rc;
+}
+
+bool async_eligible(const Ctx &c) {
+  const int nsteps = (int)c.plan->steps.size();
+  if (c.table || c.stop_at >= 0 || nsteps < 2) return false;
+  for (int si = 0; si + 1 < nsteps; ++si)
+    if (!row_serial_step(c.dsteps[(size_t)si], *c.g)) return false;  // atomic-reservation kernels
+  return true;
+}
+
+// done = true when the match completed on this path (count in c.d_acc, stats filled)
+dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows, int64_t seed_base,
+                    bool &done) {
+  done = false;
+  const int nsteps = (int)c.plan->steps.size();
+  std::vector<uint64_t> cap((size_t)nsteps, 0);
+  std::vector<int> words((size_t)nsteps, 0);
+  double expect = (double)seed_rows;
+  uint64_t cap_in = (uint64_t)seed_rows, prev_bytes = 0;
+  const uint64_t avail =
+      c.mem_budget ? c.mem_budget : (c.mem_total > c.live ? (c.mem_total - c.live) / 2 : 0);
+  for (int si = 0; si + 1 < nsteps; ++si) {
+    const DevStep &D = c.dsteps[(size_t)si];
+    if (ratio[(size_t)si] <= 0) return DM_OK;
+    expect *= ratio[(size_t)si];
+    cap[(size_t)si] = (uint64_t)(expect * 1.15) + 4096;
+    words[(size_t)si] = row_words(D.in_w + D.n_new, level_elem(c, si + 1));
+    const uint64_t bytes = cap[(size_t)si] * (uint64_t)words[(size_t)si] * 4u;
+    if (bytes + prev_bytes > 2 * avail) return DM_OK;  // two live levels must fit the budget
+    prev_bytes = bytes;
+  }
+  DevBuf<unsigned long long> ctrl;
+  CK(ctrl.alloc((size_t)3 * nsteps, c.s), "ctrl");
+  CK(cudaMemsetAsync(ctrl.p, 0, sizeof(unsigned long long) * 3 * nsteps, c.s), "memset");
+  int32_t *in = nullptr;
+  const unsigned long long *d_in = nullptr;
+  for (int si = 0; si < nsteps; ++si) {
+    const DevStep &D = c.dsteps[(size_t)si];
+    const bool last = si == nsteps - 1;
+    const int64_t tiles = (int64_t)((cap_in + kTileRows - 1) / kTileRows);
+    StepIO io{};
+    io.in = in;
+    io.in_rows = (int64_t)cap_in;
+    io.d_in_rows = d_in;
+    io.seed_base = si == 0 ? seed_base : 0;
+    io.elem = level_elem(c, si);
+    io.out_elem = level_elem(c, si + 1);
+    io.stats = c.d_acc + kAccSlots + 2 * kAccSlots * si;
+    c.st.num_chunks++;
+    if (last) {
+      io.total = c.d_acc;
+      Prof::Ev e;
+      c.prof.begin(si, 0, e);
+      const int pm = pair_mode_of(D);
+      if (pm >= 0 && !row_serial_step(D, *c.g))
+        CK(launch_pairs(D, io, *c.g, pm, c.s), "pair kernel");
+      else
+        CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
+      c.prof.end(e);
+      c.st.num_launches++;
+    } else {
+      int32_t *out = nullptr;
+      unsigned long long *agg = nullptr;
+      CK(cudaMallocAsync((void **)&out, sizeof(int32_t) * (size_t)cap[(size_t)si] * words[(size_t)si], c.s),
+         "frontier allocation");
+      CK(cudaMallocAsync((void **)&agg, sizeof(unsigned long long) * (size_t)(tiles + 1), c.s), "agg");
+      io.out = out;
+      io.cap = cap[(size_t)si];
+      io.ctrl = ctrl.p + 3 * si;
+      io.agg = agg;
+      Prof::Ev e;
+      c.prof.begin(si, 1, e);
+      cudaError_t err = launch_step_single(D, io, *c.g, tiles, c.s);
+      c.prof.end(e);
+      c.st.num_launches++;
+      cudaFreeAsync(agg, c.s);
+      if (in) cudaFreeAsync(in, c.s);  // stream-ordered: after the kernel that read it
+      if (err != cudaSuccess) {
+        cudaFreeAsync(out, c.s);
+        return cuda_fail(err, "single-pass kernel");
+      }
+      in = out;
+      d_in = ctrl.p + 3 * si + 2;
+      cap_in = cap[(size_t)si];
+    }
+  }
+  if (in) cudaFreeAsync(in, c.s);
+  std::vector<unsigned long long> h((size_t)3 * nsteps);
+  CK(cudaMemcpyAsync(h.data(), ctrl.p, sizeof(unsigned long long) * 3 * nsteps, cudaMemcpyDeviceToHost, c.s),
+     "D2H ctrl");
+  CK(cudaStreamSynchronize(c.s), "sync");
+  for (int si = 0; si + 1 < nsteps; ++si)
+    if (h[(size_t)3 * si + 1] != 0) return DM_OK;  // a level outgrew its capacity: re-run
+  uint64_t rows = (uint64_t)seed_rows;
+  for (int si = 0; si < nsteps; ++si) {
+    c.st.rows_in[si] = rows;
+    if (si + 1 < nsteps) {
+      c.st.rows_out[si] = h[(size_t)3 * si + 2];
+      c.ratio[(size_t)si] = rows ? (double)c.st.rows_out[si] / (double)rows : 0.0;
+      rows = c.st.rows_out[si];
+    }
+  }
+  c.st.pipelined = 1;
+  done = true;
+  return DM_OK;
+}
+
 // Permute columns to pattern order and sort rows lexicographically (LSD radix sort over the
 // columns, last column first).  Writes host rows.
 dm_status canonicalize(Ctx &c, int32_t *host_out) {
@@ -696,8 +826,42 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     }
   } else {
     tr("before steps");
-    if (from_step > 0) stt = run_step(c, from_step, from_rows, from_n, 0);
-    else stt = run_step(c, 0, nullptr, se - sb, sb);
+    // sync-free path for a repeated count query (growth ratios of the previous identical run)
+    char kb[96];
+    std::snprintf(kb, sizeof(kb), "%llu|%d|%d|%d|%lld|%lld|%d|", (unsigned long long)g->gen, k,
+                  opt.mode, opt.motifs, (long long)sb, (long long)se, c.elem);
+    std::string rkey(kb);
+    if (pm > 0) rkey.append(reinterpret_cast<const char *>(p_edges), (size_t)pm * 2 * sizeof(int32_t));
+    bool done = false;
+    if (from_step == 0 && async_eligible(c)) {
+      std::vector<double> rat;
+      {
+        RatioCache &rc = ratio_cache();
+        std::lock_guard<std::mutex> lk(rc.mu);
+        auto it = rc.m.find(rkey);
+        if (it != rc.m.end()) rat = it->second;
+      }
+      if (!rat.empty()) {
+        stt = run_async(c, rat, se - sb, sb, done);
+        if (stt != DM_OK) return stt;
+        if (!done) {  // fall back: clear the partial counters and statistics
+          CK(cudaMemsetAsync(c.d_acc, 0, sizeof(unsigned long long) * nacc, c.s), "memset");
+          for (int i = 0; i < nst; ++i) c.st.rows_in[i] = c.st.rows_out[i] = 0;
+          c.st.num_launches = c.st.num_chunks = 0;
+          c.prof.reset();
+        }
+      }
+    }
+    if (!done) {
+      if (from_step > 0) stt = run_step(c, from_step, from_rows, from_n, 0);
+      else stt = run_step(c, 0, nullptr, se - sb, sb);
+    }
+    if (stt == DM_OK && from_step == 0 && async_eligible(c)) {
+      RatioCache &rc = ratio_cache();
+      std::lock_guard<std::mutex> lk(rc.mu);
+      if (rc.m.size() > 4096) rc.m.clear();
+      rc.m[rkey] = c.ratio;
+    }
     tr("steps");
     if (stt != DM_OK) {
       if (c.d_front) cudaFreeAsync(c.d_front, c.s);

@@ -18,9 +18,11 @@ namespace {
 // or, for longer anchor lists, in a per-warp global slab of max_degree entries.
 template <int NQ>
 __global__ void __launch_bounds__(kStepThreads)
-    k_pairs(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+    k_pairs(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
             const int32_t *__restrict__ adj, int32_t *__restrict__ slab, int64_t slab_cap,
             int pair_mode, unsigned long long *__restrict__ row_counter) {
+  StepIO io = io_;  // device-written input size (sync-free chaining)
+  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
   constexpr int kWarps = kStepThreads / 32;
   __shared__ __align__(16) int32_t s_row[kWarps][64];
   __shared__ int32_t s_list[kWarps][kPairSmem];
@@ -182,7 +184,7 @@ int pair_mode_of(const DevStep &st) {
 
 cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g, int pair_mode,
                          cudaStream_t s) {
-  if (io.in_rows <= 0) return cudaSuccess;
+  if (io.in_rows <= 0 && !io.d_in_rows) return cudaSuccess;
   auto kern = k_pairs<0>;
   switch (row_stride(st.in_w) >> 2) {
     case 1: kern = k_pairs<1>; break;

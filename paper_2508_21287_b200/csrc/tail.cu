@@ -89,8 +89,10 @@ __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *ro
 // depth-first enumeration (dfs_ell), CTA-reduced counters.
 template <int NQ>
 __global__ void __launch_bounds__(kStepThreads)
-    k_deep(const DevStep st, const StepIO io, const int64_t *__restrict__ off,
+    k_deep(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
+  StepIO io = io_;  // device-written input size (sync-free chaining)
+  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t s_bar;
   const int w = st.in_w, ws = row_stride(w), ss = smem_stride(w);
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kStepThreads)
 
 cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
                         cudaStream_t s) {
-  if (io.in_rows <= 0 || tiles <= 0) return cudaSuccess;
+  if ((io.in_rows <= 0 && !io.d_in_rows) || tiles <= 0) return cudaSuccess;
   StepIO io2 = io;
   io2.ell = g.d_ell;
   const size_t smem = sizeof(int32_t) * (size_t)kTileRows * smem_stride(st.in_w);

@@ -285,6 +285,34 @@ def test_deep_tail_counts(dm, graph):
     assert deep >= 4
 
 
+def test_pipelined_repeat_queries(dm):
+    """A repeated count query is enqueued without per-step host synchronisation (capacities
+    from the previous identical run, sizes read on the device) when every materializing step
+    runs in the row-serial kernel (max degree <= 4 here; the others stay on the synchronising
+    path): counts and per-step row statistics must equal the first run and the oracle, for
+    several graphs, patterns, modes and seed ranges."""
+    cases = [(g.ibm_heavy_hex(10), g.path(16), "mono", None), (g.ibm_heavy_hex(10), g.ring(12), "induced", None),
+             (g.grid(60), g.path(8), "mono", (100, 2000)), (g.grid_diag(40), g.ring(5), "mono", None),
+             (g.er_gnm(2000, 6000, 3), g.path(6), "induced", None)]
+    for (n, e), (k, pe), mode, seeds in cases:
+        G = dm.Graph(n, e)
+        kw = {"seed_range": seeds} if seeds else {}
+        first = G.match(k, pe, mode=mode, profile=True, **kw)
+        assert not first.stats["pipelined"]
+        if seeds:  # a seed shard: the first (synchronising) run is the reference
+            want = first.count
+        else:
+            want = oracle.match(n, e, k, pe, induced=(mode == "induced"), table=False).count
+            assert first.count == want
+        for _ in range(2):
+            r = G.match(k, pe, mode=mode, profile=True, **kw)
+            assert r.count == want
+            assert r.stats["rows_out"][:-1] == first.stats["rows_out"][:-1]
+            assert r.stats["candidates"] == first.stats["candidates"]
+        if G.max_degree <= 4 and first.stats["num_steps"] > 1:  # every step row-serial
+            assert r.stats["pipelined"], (k, mode)
+
+
 def test_config5_random_subgraphs(dm):
     n, e = g.ibm_heavy_hex(31)
     G = dm.Graph(n, e)
