@@ -27,7 +27,8 @@ __device__ __forceinline__ int32_t colval4(const int32_t *row, int w, int c, con
 
 template <int J, int NQ>
 __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *row, int w, int ws,
-                                            unsigned long long bloom, int32_t (&x)[kMaxNew],
+                                            unsigned long long bloom, int2 tail2,
+                                            int32_t (&x)[kMaxNew],
                                             const int4 *__restrict__ ell, uint32_t &cand,
                                             uint32_t &probes) {
   if constexpr (J >= kMaxNew) {
@@ -64,7 +65,13 @@ __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *ro
 #pragma unroll
       for (int t = 0; t < J; ++t) ok &= x[t] != y;  // distinct from the other new vertices
       if (!ok) continue;
-      if ((bloom & bloom_bit(y)) && in_row_q<NQ>(row, ws, y)) continue;  // ... and from the row
+      // ... and from the row: the two most recent columns first (for the first two new
+      // vertices they hold the anchor's own predecessors, which every list contains), then
+      // the Bloom filter and the exact scan
+      if constexpr (J < 2) {
+        if (y == tail2.x || y == tail2.y) continue;
+      }
+      if ((bloom & bloom_bit(y)) && in_row_q<NQ>(row, ws, y)) continue;
       if (extra) {
         for (int t = 0; t < st.n_nbr[J] && ok; ++t) {
           const int c = st.nbr[J][t];
@@ -79,7 +86,7 @@ __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *ro
         if (!ok) continue;
       }
       x[J] = y;
-      tot += dfs_ell<J + 1, NQ>(st, row, w, ws, bloom, x, ell, cand, probes);
+      tot += dfs_ell<J + 1, NQ>(st, row, w, ws, bloom, tail2, x, ell, cand, probes);
     }
     return tot;
   }
@@ -110,7 +117,7 @@ __global__ void __launch_bounds__(kStepThreads)
     const int32_t *row = rows + tid * ss;
     unsigned long long bloom = 0;
     for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
-    ns = dfs_ell<0, NQ>(st, row, w, ws, bloom, x, reinterpret_cast<const int4 *>(io.ell), my_cand,
+    ns = dfs_ell<0, NQ>(st, row, w, ws, bloom, make_int2(row[w - 1], w >= 2 ? row[w - 2] : -1), x, reinterpret_cast<const int4 *>(io.ell), my_cand,
                         my_probe);
   }
   unsigned long long v3[3] = {my_cand, my_probe, ns};
