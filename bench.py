@@ -326,6 +326,12 @@ def main():
             "bytes_model_per_embedding": total_model / max(1.0, float(count))}
     if isinstance(traffic, dict):
         roof["traffic_source"] = traffic.get("source")
+    # every launch kind (the count-only tail and the materializing single pass take similar time
+    # on config 5): model GB/s and fraction of the measured peak per kind
+    roof["by_kind"] = {kk: {"ms": v[0], "launches": v[2],
+                            "achieved_GBps": (v[1] / 1e9) / (v[0] / 1e3) if v[0] > 0 else 0.0,
+                            "frac": ((v[1] / 1e9) / (v[0] / 1e3)) / peak if v[0] > 0 else 0.0}
+                       for kk, v in kinds.items() if v[2] > 0}
 
     # ---------------- end to end through the public API from pinned host buffers
     e2e_val = None

@@ -491,6 +491,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
       const int4 *ell = reinterpret_cast<const int4 *>(io.ell);
       unsigned long long bloom = 0;
       for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
+      const int2 tail2 = make_int2(row[w - 1], w >= 2 ? row[w - 2] : -1);
       int4 na;
       const int ac = pick_anchor_ell(st, 0, row, w, 0, ell, na);
 #pragma unroll
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
         const int32_t x0 = ell_at(na, i);
         if (x0 < 0) break;
         ++n_cand;
-        if (!accept_ell<NQ>(st, 0, row, w, ws, bloom, 0, x0, ac, ell, n_probe)) continue;
+        if (!accept_ell<NQ>(st, 0, row, w, ws, bloom, tail2, 0, x0, ac, ell, n_probe)) continue;
         if (st.n_new == 1) {
           on_survivor(x0, -1);
           continue;
@@ -510,7 +511,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
           const int32_t x1 = ell_at(nb, i1);
           if (x1 < 0) break;
           ++n_cand;
-          if (accept_ell<NQ>(st, 1, row, w, ws, bloom, x0, x1, bc, ell, n_probe)) on_survivor(x0, x1);
+          if (accept_ell<NQ>(st, 1, row, w, ws, bloom, tail2, x0, x1, bc, ell, n_probe)) on_survivor(x0, x1);
         }
       }
     } else {

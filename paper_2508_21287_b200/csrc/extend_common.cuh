@@ -296,12 +296,16 @@ __device__ __forceinline__ int pick_anchor_ell(const DevStep &st, int j, const i
   return best;
 }
 
+// tail2 = the row's last two columns: compared before the Bloom test because the anchor's
+// predecessors (always in its list) sit there for path-like joins -- a certain Bloom hit and
+// exact scan otherwise
 template <int NQ>
 __device__ __forceinline__ bool accept_ell(const DevStep &st, int j, const int32_t *row, int w,
-                                           int ws, unsigned long long bloom, int32_t x0, int32_t x,
-                                           int acol, const int4 *__restrict__ ell,
-                                           uint32_t &probes) {
+                                           int ws, unsigned long long bloom, int2 tail2,
+                                           int32_t x0, int32_t x, int acol,
+                                           const int4 *__restrict__ ell, uint32_t &probes) {
   if (j == 1 && x == x0) return false;
+  if (x == tail2.x || x == tail2.y) return false;
   if ((bloom & bloom_bit(x)) && in_row_q<NQ>(row, ws, x)) return false;
   if (st.n_nbr[j] <= 1 && st.n_non[j] == 0) return true;
   for (int t = 0; t < st.n_nbr[j]; ++t) {
