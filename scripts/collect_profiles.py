@@ -12,6 +12,7 @@ for f in glob.glob("gpurun_out/bench_*.json"):
 out = [f"# {tag} ncu summaries\n"]
 for f in sorted(glob.glob("gpurun_out/launches_*.csv")):
     wl = os.path.basename(f)[len("launches_"):-4]
+    open(f"profiles/{tag}_launches_{wl}.csv", "w").write(open(f).read())  # the raw launch list
     r = subprocess.run([sys.executable, "scripts/ncu_traffic.py", f, wl], capture_output=True, text=True)
     out += [f"## launch list {wl} (ncu --metrics gpu__time_duration.sum,dram__bytes_*; one dm_match)", "```", r.stdout.strip(), "```", ""]
 want = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Executed Ipc Active",
