@@ -70,32 +70,36 @@ __global__ void __launch_bounds__(kStepThreads)
       // ---- every ordered pair of S
       const int64_t np = (int64_t)ns * ns;
       if (lane == 0 && pair_mode != 1) cand += (unsigned long long)np;
+      // 4-clique closing probe: the ranges of N(x0) inside [min S, max S] are found for 32
+      // first vertices at once (one bisection chain per lane, in parallel) and broadcast
+      int64_t my_lo = 0, my_hi = 0;
       for (int i = 0; i < ns; ++i) {
         const int32_t x0 = S[i];
         if (pair_mode == 1 && ns > 1) {
-          // x1 in S with (x0, x1) in E: join S with N(x0) restricted to [S[0], S[ns-1]],
-          // iterating the smaller side and binary-searching the other (S is sorted)
-          const int64_t b = __ldg(off + x0), e = __ldg(off + x0 + 1);
-          int64_t lo = b, hi = e;
-          {
-            const int32_t smin = S[0];
-            int64_t l = b, h = e;
-            while (l < h) {
-              const int64_t m = (l + h) >> 1;
-              if (__ldg(adj + m) < smin) l = m + 1;
-              else h = m;
+          if ((i & 31) == 0) {
+            const int ii = i + lane;
+            if (ii < ns) {
+              const int32_t xx = S[ii];
+              const int64_t b = __ldg(off + xx), e = __ldg(off + xx + 1);
+              const int32_t smin = S[0], smax = S[ns - 1];
+              int64_t l = b, h = e;
+              while (l < h) {
+                const int64_t m = (l + h) >> 1;
+                if (__ldg(adj + m) < smin) l = m + 1;
+                else h = m;
+              }
+              my_lo = l;
+              h = e;
+              while (l < h) {
+                const int64_t m = (l + h) >> 1;
+                if (__ldg(adj + m) <= smax) l = m + 1;
+                else h = m;
+              }
+              my_hi = l;
             }
-            lo = l;
-            const int32_t smax = S[ns - 1];
-            l = lo;
-            h = e;
-            while (l < h) {
-              const int64_t m = (l + h) >> 1;
-              if (__ldg(adj + m) <= smax) l = m + 1;
-              else h = m;
-            }
-            hi = l;
           }
+          const int64_t lo = __shfl_sync(0xffffffffu, my_lo, i & 31);
+          const int64_t hi = __shfl_sync(0xffffffffu, my_hi, i & 31);
           const int64_t m = hi - lo;
           if (lane == 0) cand += (unsigned long long)(m <= 2 * (int64_t)ns ? m : ns);
           if (m <= 2 * (int64_t)ns) {
