@@ -115,10 +115,24 @@ __global__ void __launch_bounds__(kStepThreads)
               cnt += (l < ns && S[l] == y);
             }
           } else {
-            for (int j = lane; j < ns; j += 32) {  // S side, probe N(x0)
-              const int32_t x1 = S[j];
-              if (j == i) continue;
-              int64_t l = lo, h = hi;
+            // S side, probe N(x0): 32 splitters of N(x0)[lo, hi) (one load per lane) give
+            // every probe its 1/32 bucket by register shuffles, so each bisection in global
+            // memory starts 5 levels down
+            const int32_t sp = __ldg(adj + lo + ((m * lane) >> 5));
+            for (int j0 = 0; j0 < ns; j0 += 32) {
+              const int j = j0 + lane;
+              const bool valid = j < ns && j != i;
+              const int32_t x1 = j < ns ? S[j] : 0;
+              int c = 0;  // number of splitters < x1
+#pragma unroll
+              for (int sft = 16; sft >= 1; sft >>= 1) {
+                const int32_t v = __shfl_sync(0xffffffffu, sp, c + sft - 1);
+                if (v < x1) c += sft;
+              }
+              if (__shfl_sync(0xffffffffu, sp, c & 31) < x1 && c == 31) c = 32;
+              if (!valid) continue;
+              int64_t l = c == 0 ? lo : lo + ((m * (c - 1)) >> 5) + 1;
+              int64_t h = c == 32 ? hi : lo + ((m * c) >> 5);
               while (l < h) {
                 const int64_t mid = (l + h) >> 1;
                 if (__ldg(adj + mid) < x1) l = mid + 1;
