@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(kStepThreads)
       // ---- every ordered pair of S
       const int64_t np = (int64_t)ns * ns;
       if (lane == 0 && pair_mode != 1) cand += (unsigned long long)np;
+      // 32 splitters of S in registers (lane k: S[ns*k/32]) for the bisections into S
+      const int32_t ssp = (pair_mode == 1 && ns > 1) ? S[(ns * lane) >> 5] : 0;
       // 4-clique closing probe: the ranges of N(x0) inside [min S, max S] are found for 32
       // first vertices at once (one bisection chain per lane, in parallel) and broadcast
       int64_t my_lo = 0, my_hi = 0;
@@ -103,9 +105,19 @@ __global__ void __launch_bounds__(kStepThreads)
           const int64_t m = hi - lo;
           if (lane == 0) cand += (unsigned long long)(m <= 2 * (int64_t)ns ? m : ns);
           if (m <= 2 * (int64_t)ns) {
-            for (int64_t t = lo + lane; t < hi; t += 32) {  // N(x0) side, probe S
-              const int32_t y = __ldg(adj + t);
-              int l = 0, h = ns;
+            for (int64_t t0 = lo; t0 < hi; t0 += 32) {  // N(x0) side, probe S
+              const int64_t t = t0 + lane;
+              const int32_t y = t < hi ? __ldg(adj + t) : 0;
+              int c = 0;  // S splitters (registers, one per lane) below y
+#pragma unroll
+              for (int sft = 16; sft >= 1; sft >>= 1) {
+                const int32_t v = __shfl_sync(0xffffffffu, ssp, c + sft - 1);
+                if (v < y) c += sft;
+              }
+              if (__shfl_sync(0xffffffffu, ssp, c & 31) < y && c == 31) c = 32;
+              if (t >= hi) continue;
+              int l = c == 0 ? 0 : ((ns * (c - 1)) >> 5) + 1;
+              int h = c == 32 ? ns : ((ns * c) >> 5);
               while (l < h) {
                 const int mid = (l + h) >> 1;
                 if (S[mid] < y) l = mid + 1;
