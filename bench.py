@@ -326,6 +326,10 @@ def main():
             "bytes_model_per_embedding": total_model / max(1.0, float(count))}
     if isinstance(traffic, dict):
         roof["traffic_source"] = traffic.get("source")
+        # ncu DRAM bytes / algorithmic bytes of the dominant kind (1 = no re-reads;
+        # < 1: L2 hits on small levels, > 1: wasted traffic)
+        if roof["algorithmic_bytes_per_launch"] > 0:
+            roof["amplification"] = roof["traffic"] / roof["algorithmic_bytes_per_launch"]
     # every launch kind (the count-only tail and the materializing single pass take similar time
     # on config 5): model GB/s and fraction of the measured peak per kind
     roof["by_kind"] = {kk: {"ms": v[0], "launches": v[2],
