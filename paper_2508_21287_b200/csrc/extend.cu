@@ -466,7 +466,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
   int32_t *sv_x = rows + kTileRows * ss;         // [kTileRows * S][2]
   int32_t *map = sv_x + 2 * kTileRows * S;       // [kTileRows * S]
 
-  load_tile(rows, ss, ws, io, r0, nrows, &s_bar);
+  load_tile<NQ>(rows, ss, ws, io, r0, nrows, &s_bar);
 
   int ns = 0;
   bool ovf = false;

@@ -119,6 +119,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
 // Tile of nrows frontier rows -> shared memory at stride ss.  Contiguous case (ss == ws): one
 // TMA bulk copy completing on an mbarrier; padded case: 16-byte cp.async per chunk, one warp
 // per row.  Implicit seed: row r = vertex seed_base + r0 + r.  Ends with a CTA barrier.
+// NQ > 0: ws == 4*NQ known at compile time (the 16-bit widening then divides by a constant)
+template <int NQ = 0>
 __device__ __forceinline__ void load_tile(int32_t *rows, int ss, int ws, const StepIO &io,
                                           int64_t r0, int nrows, uint64_t *bar) {
   const int tid = threadIdx.x;
@@ -132,7 +134,7 @@ __device__ __forceinline__ void load_tile(int32_t *rows, int ss, int ws, const S
   }
   if (io.elem == 2) {  // 16-bit rows: 16-byte loads of 8 ids, widened to int32 in shared memory
     const int s16 = row_stride16(ws > 0 ? ws : 1);  // ws is row_stride(w); chunks of 8 ids
-    const int nq8 = s16 >> 3;
+    const int nq8 = NQ > 0 ? (NQ + 1) / 2 : s16 >> 3;
     const uint4 *src16 = reinterpret_cast<const uint4 *>(
         reinterpret_cast<const uint16_t *>(io.in) + (int64_t)r0 * s16);
     const int total = nrows * nq8;  // chunks of the tile are contiguous in global memory

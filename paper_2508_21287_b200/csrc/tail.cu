@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kStepThreads)
   if (r0 >= io.in_rows) return;
   const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
   int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
-  load_tile(rows, ss, ws, io, r0, nrows, &s_bar);
+  load_tile<NQ>(rows, ss, ws, io, r0, nrows, &s_bar);
   uint32_t my_cand = 0, my_probe = 0;
   unsigned ns = 0;
   if (tid < nrows) {
