@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kStepThreads)
   }
 }
 
-// Split tail for n_new == 4: phase 1 (thread = row) enumerates x_0, x_1 and queues the
+// Split tail (n_new 3-4): phase 1 (thread = row) enumerates x_0, x_1 and queues the
 // surviving partial rows in shared memory; phase 2 spreads the queue evenly over the CTA's
 // threads, each finishing x_2, x_3 of its entries.  The per-row 4-deep recursion left 17 of 32
 // lanes idle (rows' subtrees differ); the queue rebalances the second half within the tile.
@@ -225,7 +225,7 @@ cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, 
   if ((io.in_rows <= 0 && !io.d_in_rows) || tiles <= 0) return cudaSuccess;
   StepIO io2 = io;
   io2.ell = g.d_ell;
-  const bool split = st.n_new == 4;
+  const bool split = st.n_new >= 3;  // two phases: x_0, x_1 per row, the rest per queue entry
   size_t smem = sizeof(int32_t) * (size_t)kTileRows * smem_stride(st.in_w);
   if (split) smem += (size_t)kTileRows * kTailQueuePerRow * (2 * sizeof(int32_t) + 1);
   auto kern = split ? k_deep_split<0> : k_deep<0>;
