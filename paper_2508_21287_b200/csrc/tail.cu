@@ -5,7 +5,7 @@
 // S:213), the closing-edge probes of multi-key joins (Fig. 2 C1/C2) and, in induced
 // mode, the non-edge probes.  CTA = tile of 256 rows in shared memory; thread = row; the
 // recursion is unrolled at compile time (static indices into the assigned new vertices).  For a
-// 4-vertex tail the CTA splits the recursion in two phases (k_deep_split): the first two levels
+// 3-4 vertex tail the CTA splits the recursion in two phases (k_deep_split): the first two levels
 // per row, their surviving partial rows queued in shared memory, the last two levels per queue
 // entry spread evenly over the threads (P30: 5.62 -> 5.16 ms).
 //
@@ -29,7 +29,7 @@ __device__ __forceinline__ int32_t colval4(const int32_t *row, int w, int c, con
 }
 
 // Shared-memory queue of partial rows (row in tile, x_0, x_1) handed from the first two tail
-// levels to the last two (split tail, n_new == 4).
+// levels to the rest (split tail, n_new 3-4).
 struct TailQueue {
   int *n;           // entries claimed (may exceed cap)
   int cap;
@@ -113,47 +113,6 @@ __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *ro
   }
 }
 
-// Deep count-only last step (3-4 new vertices, ELL graphs): tile -> smem, one thread per row,
-// depth-first enumeration (dfs_ell), CTA-reduced counters.
-template <int NQ>
-__global__ void __launch_bounds__(kStepThreads)
-    k_deep(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
-           const int32_t *__restrict__ adj) {
-  StepIO io = io_;  // device-written input size (sync-free chaining)
-  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ __align__(8) uint64_t s_bar;
-  const int w = st.in_w, ws = row_stride(w), ss = smem_stride(w);
-  const int tid = threadIdx.x;
-  const int64_t tile = io.block_begin + blockIdx.x;
-  const int64_t r0 = tile * kTileRows;
-  if (r0 >= io.in_rows) return;
-  const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
-  int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
-  load_tile<NQ>(rows, ss, ws, io, r0, nrows, &s_bar);
-  uint32_t my_cand = 0, my_probe = 0;
-  unsigned ns = 0;
-  if (tid < nrows) {
-    int32_t x[kMaxNew] = {-1, -1, -1, -1};
-    const int32_t *row = rows + tid * ss;
-    unsigned long long bloom = 0;
-    for (int c = 0; c < w; ++c) bloom |= bloom_bit(row[c]);
-    ns = dfs_ell<0, NQ>(st, row, w, ws, bloom, make_int2(row[w - 1], w >= 2 ? row[w - 2] : -1), x, reinterpret_cast<const int4 *>(io.ell), my_cand,
-                        my_probe);
-  }
-  unsigned long long v3[3] = {my_cand, my_probe, ns};
-  block_sum3(v3);
-  if (tid == 0) {
-    const int slot = (int)(tile & (kAccSlots - 1));
-    if (io.stats) {
-      atomicAdd(io.stats + slot, v3[0]);
-      atomicAdd(io.stats + kAccSlots + slot, v3[1]);
-    }
-    if (io.block_cnt) io.block_cnt[tile] = v3[2];
-    if (io.total && v3[2]) atomicAdd(io.total + slot, v3[2]);
-  }
-}
-
 // Split tail (n_new 3-4): phase 1 (thread = row) enumerates x_0, x_1 and queues the
 // surviving partial rows in shared memory; phase 2 spreads the queue evenly over the CTA's
 // threads, each finishing x_2, x_3 of its entries.  The per-row 4-deep recursion left 17 of 32
@@ -225,19 +184,18 @@ cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, 
   if ((io.in_rows <= 0 && !io.d_in_rows) || tiles <= 0) return cudaSuccess;
   StepIO io2 = io;
   io2.ell = g.d_ell;
-  const bool split = st.n_new >= 3;  // two phases: x_0, x_1 per row, the rest per queue entry
-  size_t smem = sizeof(int32_t) * (size_t)kTileRows * smem_stride(st.in_w);
-  if (split) smem += (size_t)kTileRows * kTailQueuePerRow * (2 * sizeof(int32_t) + 1);
-  auto kern = split ? k_deep_split<0> : k_deep<0>;
+  size_t smem = sizeof(int32_t) * (size_t)kTileRows * smem_stride(st.in_w) +
+                (size_t)kTileRows * kTailQueuePerRow * (2 * sizeof(int32_t) + 1);
+  auto kern = k_deep_split<0>;
   switch (row_stride(st.in_w) >> 2) {
-    case 1: kern = split ? k_deep_split<1> : k_deep<1>; break;
-    case 2: kern = split ? k_deep_split<2> : k_deep<2>; break;
-    case 3: kern = split ? k_deep_split<3> : k_deep<3>; break;
-    case 4: kern = split ? k_deep_split<4> : k_deep<4>; break;
-    case 5: kern = split ? k_deep_split<5> : k_deep<5>; break;
-    case 6: kern = split ? k_deep_split<6> : k_deep<6>; break;
-    case 7: kern = split ? k_deep_split<7> : k_deep<7>; break;
-    case 8: kern = split ? k_deep_split<8> : k_deep<8>; break;
+    case 1: kern = k_deep_split<1>; break;
+    case 2: kern = k_deep_split<2>; break;
+    case 3: kern = k_deep_split<3>; break;
+    case 4: kern = k_deep_split<4>; break;
+    case 5: kern = k_deep_split<5>; break;
+    case 6: kern = k_deep_split<6>; break;
+    case 7: kern = k_deep_split<7>; break;
+    case 8: kern = k_deep_split<8>; break;
     default: break;
   }
   // Shared memory only for the register-limited number of resident CTAs; the rest of the
