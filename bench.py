@@ -143,7 +143,7 @@ def cpu_baseline(n, e, k, pe, drop, target_s=12.0):
             "kind": "oracle",
             "sample": f"roots f(v{int(r.order[0])}) in [0,{R}) of {n} data vertices "
                       f"({100.0 * R / max(n, 1):.1f}% of the root set): {r.count} embeddings "
-                      f"in {r.seconds:.2f}s on {r.threads} threads"}, r
+                      f"in {r.seconds:.2f}s on {r.threads} threads"}, r, R
 
 
 def run_reference(args, wl):
@@ -155,7 +155,7 @@ def run_reference(args, wl):
     n, e = gfn()
     k, pe = pfn()
     per_step = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
-    base, _ = cpu_baseline(n, e, k, pe, drop, target_s=per_step)
+    base, _, _ = cpu_baseline(n, e, k, pe, drop, target_s=per_step)
     vals = []
     import oracle
     R = int(base["sample"].split("[0,")[1].split(")")[0])
@@ -199,7 +199,7 @@ def main():
     import torch.distributed as tdist
 
     import paper_2508_21287_b200 as dm
-    from paper_2508_21287_b200.dist import equal_work_cuts
+    from paper_2508_21287_b200.dist import rebalance_rows, reduce_count
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -225,10 +225,9 @@ def main():
     t0 = time.perf_counter()
     G = dm.Graph(n, e, drop_self_loops=drop, device=local)
     prep_s = time.perf_counter() - t0
-    off, _ = G.csr()
-    cuts = equal_work_cuts(off, world)
+    plan = G.plan(k, pe)                     # the plan dm_match executes (dm_plan_create_for)
+    cuts = plan.seed_cuts(G, world)          # equal-work seed ranges (library)
     seed = (cuts[rank], cuts[rank + 1])
-    plan = dm.Plan(k, pe, stats=G.stats(count_only=True))   # the plan dm_match builds
     flush = torch.empty(int(300e6) // 4, dtype=torch.int32, device="cuda")  # > 126 MB L2
 
     def barrier():
@@ -248,31 +247,53 @@ def main():
 
     def one(profile=False):
         if dist_on and rebalance_step > 0:
-            from paper_2508_21287_b200.dist import rebalance_rows
             fr = G.match_prefix(k, pe, rebalance_step, seed_range=seed, stream=stream)
-            mine = rebalance_rows(fr.rows_tensor(), fr.work_tensor(), rank=rank, world=world)
-            return G.match_resume(k, pe, rebalance_step, mine, stream=stream, profile=profile)
-        return G.match(k, pe, seed_range=seed, stream=stream, profile=profile)
+            mine = rebalance_rows(fr.rows_tensor(), fr.work_tensor(), fr.work_total, rank=rank,
+                                  world=world, coll_device=torch.device(coll_dev), stream=stream)
+            r = G.match_resume(k, pe, rebalance_step, mine, stream=stream, profile=profile)
+        else:
+            r = G.match(k, pe, seed_range=seed, stream=stream, profile=profile)
+        # C3: the job's count, all_reduced inside the timed step
+        total = reduce_count(r.count, coll_device=torch.device(coll_dev)) if dist_on else r.count
+        return r, total
 
     for _ in range(max(3, args.warmup)):
         one()
     barrier()
+    # cold query (after the warm-up, so kernels are loaded): the first dm_match on a freshly created graph (no growth-ratio cache, so every
+    # level size is read back before the next step is launched), device-timed
+    Gc = dm.Graph(n, e, drop_self_loops=drop, device=local)
+    barrier()
+    ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ca.record(stream)
+    rc = Gc.match(k, pe, seed_range=seed, stream=stream)
+    cb.record(stream)
+    barrier()
+    cold_ms = ca.elapsed_time(cb)
+    Gc.close()
+
     clk = ClockSampler(local)
     clk.start()
-    times, stats, count = [], [], 0
+    times, stats, count, totals = [], [], 0, []
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     barrier()
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        r = one(profile=True)
+        r, tot = one(profile=True)
         ev[i][1].record(stream)
         count += r.count
+        totals.append(tot)
         stats.append(r.stats)
     barrier()
     clocks = clk.stop()
     times = [a.elapsed_time(b) for a, b in ev]
+    # every timed step must find the same embeddings (and the cold query the same local count)
+    if len(set(totals)) != 1:
+        raise SystemExit(f"bench: per-step counts differ: {sorted(set(totals))}")
+    if not (dist_on and rebalance_step > 0) and rc.count != r.count:
+        raise SystemExit(f"bench: cold query found {rc.count} embeddings, timed steps {r.count}")
     if os.environ.get("DM_BENCH_DEBUG"):
         print("step ms:", [round(t, 2) for t in times], "kernel ms:", [round(sum(s["ms_count"]) + sum(s["ms_write"]), 2) for s in stats], file=sys.stderr)
     local_ms = float(sum(times))
@@ -288,54 +309,65 @@ def main():
     value = total_count / (max_ms / 1000.0)
 
     # ---------------- roofline of the dominant kernel (SURVEY §8(d) byte model)
-    # Launch kinds: "single" = the fused join step of every materialized level (single pass:
-    # join + filters + look-back prefix + write), "count" = the count-only last step.  Bytes per
-    # launch follow SURVEY §8(d) with the stored id width e (4, or 2 for 16-bit levels): read
-    # rows e*w*|F_i| (0 for the implicit seed) + key lookups 8*|F_i| + candidates 4*C_i + probes
-    # 4*Q_i (+ write e*w_{i+1}*|F_{i+1}| for "single").
-    kinds = {"join_single": [0.0, 0.0, 0], "join_count": [0.0, 0.0, 0]}
+    # Launch kinds: "join_single" = the fused join step of every materialized level (join +
+    # filters + single-pass compaction + write), "join_count" = the count-only last step.
+    # frac: SURVEY §8(d) as written (4 B per id, the seed's one-column read included):
+    #   4 w_i |F_i| + 8 |F_i| + 4 C_i + 4 Q_i (+ 4 w_{i+1} |F_{i+1}| for materialized levels)
+    # frac_stored: the same with the stored id width (2 B for 16-bit levels, no implicit-seed read)
+    # frac_dram: ncu dram__bytes_read+write per launch of the kind (profiles/traffic.json, one
+    #   `ncu --set full` / launch-list capture of this workload) / the live CUDA-event ms per launch
+    kinds = {"join_single": [0.0, 0.0, 0, 0.0], "join_count": [0.0, 0.0, 0, 0.0]}
     for s in stats:  # per-step algorithmic bytes come from the library (dm_match_stats)
         for i in range(s["num_steps"]):
-            if s["ms_count"][i] > 0:
-                kinds["join_count"][0] += s["ms_count"][i]
-                kinds["join_count"][1] += s["bytes_model"][i]
-                kinds["join_count"][2] += 1
-            if s["ms_write"][i] > 0:
-                kinds["join_single"][0] += s["ms_write"][i]
-                kinds["join_single"][1] += s["bytes_model"][i]
-                kinds["join_single"][2] += 1
+            for kk, key in (("join_count", "ms_count"), ("join_single", "ms_write")):
+                if s[key][i] > 0:
+                    kinds[kk][0] += s[key][i]
+                    kinds[kk][1] += s["bytes_model"][i]
+                    kinds[kk][2] += 1
+                    kinds[kk][3] += s["bytes_stored"][i]
     dom = max(kinds, key=lambda kk: kinds[kk][0])
-    ms, byts, launches = kinds[dom]
+    ms, byts, launches, byts_st = kinds[dom]
     peak, peak_src = load_peaks()
     achieved = (byts / 1e9) / (ms / 1e3) if ms > 0 else 0.0
-    traffic = None
+    traffic_all = {}
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.workload, {}).get(dom)
+            traffic_all = json.load(open(tp)).get(args.workload, {}) or {}
         except Exception:
-            traffic = None
+            traffic_all = {}
+    traffic = traffic_all.get(dom)
     total_model = sum(sum(s["bytes_model"]) for s in stats)
-    roof = {"bound": "hbm", "kernel": dom + " (k_rows/k_step, extend.cu)", "achieved": achieved,
+    ms_launch = ms / max(1, launches)
+    roof = {"bound": "hbm", "kernel": dom + " (extend.cu / tail.cu / pairs.cu)", "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic["bytes_per_launch"] if isinstance(traffic, dict) else traffic,
             "algorithmic_bytes_per_launch": byts / max(1, launches),
-            "ms_per_launch": ms / max(1, launches), "launches": launches,
+            "byte_model": "SURVEY 8(d) as written: 4 B/id, seed read included",
+            "frac_stored": ((byts_st / 1e9) / (ms / 1e3)) / peak if ms > 0 else 0.0,
+            "ms_per_launch": ms_launch, "launches": launches,
             "peak_source": peak_src, "kernel_share_of_step": ms / max(1e-9, sum(times)),
             "step_model_GBps": (total_model / 1e9) / (sum(times) / 1e3),
             "bytes_model_per_embedding": total_model / max(1.0, float(count))}
     if isinstance(traffic, dict):
         roof["traffic_source"] = traffic.get("source")
+        roof["frac_dram"] = (traffic["bytes_per_launch"] / 1e9) / (ms_launch / 1e3) / peak if ms_launch > 0 else None
         # ncu DRAM bytes / algorithmic bytes of the dominant kind (1 = no re-reads;
         # < 1: L2 hits on small levels, > 1: wasted traffic)
         if roof["algorithmic_bytes_per_launch"] > 0:
             roof["amplification"] = roof["traffic"] / roof["algorithmic_bytes_per_launch"]
-    # every launch kind (the count-only tail and the materializing single pass take similar time
-    # on config 5): model GB/s and fraction of the measured peak per kind
-    roof["by_kind"] = {kk: {"ms": v[0], "launches": v[2],
-                            "achieved_GBps": (v[1] / 1e9) / (v[0] / 1e3) if v[0] > 0 else 0.0,
-                            "frac": ((v[1] / 1e9) / (v[0] / 1e3)) / peak if v[0] > 0 else 0.0}
-                       for kk, v in kinds.items() if v[2] > 0}
+    # every launch kind: model GB/s and fraction of the measured peak per kind
+    roof["by_kind"] = {}
+    for kk, v in kinds.items():
+        if v[2] == 0:
+            continue
+        d = {"ms": v[0], "launches": v[2], "achieved_GBps": (v[1] / 1e9) / (v[0] / 1e3) if v[0] > 0 else 0.0}
+        d["frac"] = d["achieved_GBps"] / peak
+        d["frac_stored"] = ((v[3] / 1e9) / (v[0] / 1e3)) / peak if v[0] > 0 else 0.0
+        tk = traffic_all.get(kk)
+        if isinstance(tk, dict) and v[0] > 0:
+            d["frac_dram"] = (tk["bytes_per_launch"] / 1e9) / ((v[0] / v[2]) / 1e3) / peak
+        roof["by_kind"][kk] = d
 
     # ---------------- end to end through the public API from pinned host buffers
     e2e_val = None
@@ -372,7 +404,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu, _ = cpu_baseline(n, e, k, pe, drop)
+        cpu, ores, R = cpu_baseline(n, e, k, pe, drop)
+        if R >= n and ores.count != totals[0]:   # the oracle covered every root
+            raise SystemExit(f"bench: oracle count {ores.count} != device count {totals[0]}")
+        cpu["matches_device_count"] = (ores.count == totals[0]) if R >= n else None
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -387,7 +422,9 @@ def main():
                           "parallelism": f"seed-shard x{world} (replicated graph)" +
                           (f", all-to-all frontier rebalance at level {rebalance_step}"
                            if dist_on and rebalance_step > 0 else ""),
-                          "prep_ms_graph_create": prep_s * 1e3},
+                          "prep_ms_graph_create": prep_s * 1e3,
+                          "cold_query_ms": cold_ms,
+                          "timed_path": "repeated query (pipelined when eligible)"},
                "roofline": roof, "cpu_baseline": cpu,
                "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": h2d,
                        "d2h_bytes_per_step": d2h},

@@ -10,7 +10,8 @@
  * graphs become edge tables, the pattern is decomposed into motif slices (§3.3),
  * and a table of partial embeddings is grown by equi-joins with the motif tables followed by
  * the overlapping-node filter (Alg. 1).  Each join step is one fused sm_100a kernel
- * pair (count, then write), see DESIGN.md.
+ * (join + filters + single-pass compaction; an exact-offset re-run only for tiles that do not
+ * fit the estimated capacity), see DESIGN.md §5.
  *
  * Conventions
  *  - Vertex ids are int32 in [0, n); counts are uint64; row offsets int64.
@@ -40,8 +41,8 @@ extern "C" {
 #define DM_API
 #endif
 
-#define DM_ABI_VERSION 2
-#define DM_MAX_PATTERN 64 /* max pattern vertices k */
+#define DM_ABI_VERSION 3
+#define DM_MAX_PATTERN 128 /* max pattern vertices k (the paper's Table 2 goes to 100) */
 
 typedef struct dm_graph dm_graph;   /* device CSR of G_d (Res(M2), both orientations) */
 typedef struct dm_result dm_result; /* count + optional canonical host table + stats   */
@@ -83,7 +84,7 @@ typedef struct {
 } dm_match_opts;
 
 /* Per-match statistics (DM_MATCH_PROFILE fills the timing fields). */
-#define DM_MAX_STEPS 64
+#define DM_MAX_STEPS 128
 typedef struct {
   int32_t num_steps;             /* executed join steps (seed included)                    */
   int32_t num_launches;          /* kernels launched by this dm_match call                 */
@@ -96,7 +97,12 @@ typedef struct {
   uint64_t probes[DM_MAX_STEPS];     /* Q_i: closing-edge / non-edge probe targets         */
   int32_t width_in[DM_MAX_STEPS];    /* w_i                                                */
   int32_t width_out[DM_MAX_STEPS];   /* w_{i+1}                                            */
-  double bytes_model[DM_MAX_STEPS];  /* SURVEY §8(d) algorithmic bytes of step i           */
+  double bytes_model[DM_MAX_STEPS];  /* SURVEY §8(d) algorithmic bytes of step i, as written:
+                                        4 B per id (seed's 1-column input included):
+                                        4 w_i |F_i| + 8 |F_i| + 4 C_i + 4 Q_i + 4 w_{i+1} |F_{i+1}|
+                                        (no write for the count-only last step)              */
+  double bytes_stored[DM_MAX_STEPS]; /* the same with the STORED id width (2 B for 16-bit levels)
+                                        and no read for the implicit seed                     */
   double ms_count[DM_MAX_STEPS];     /* device ms in count-pass kernels of step i          */
   double ms_write[DM_MAX_STEPS];     /* device ms in write-pass kernels of step i          */
   double ms_other;                   /* scans, canonical sort, copies                      */
@@ -186,10 +192,82 @@ DM_API int32_t dm_frontier_width(const dm_frontier *f);
 DM_API int32_t dm_frontier_stride(const dm_frontier *f);
 DM_API const int32_t *dm_frontier_device_rows(const dm_frontier *f);
 DM_API const uint64_t *dm_frontier_device_work(const dm_frontier *f);
+DM_API uint64_t dm_frontier_work_total(const dm_frontier *f);   /* sum of the work estimates     */
+/* Frees the frontier's buffers stream-ordered on the stream it was produced on (no device-wide
+ * synchronisation); that stream must still exist (NULL = legacy default stream). */
 DM_API void dm_frontier_free(dm_frontier *f);
 DM_API dm_status dm_match_resume(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
                                  const dm_match_opts *opt, int32_t from_step, const int32_t *d_rows,
                                  int64_t rows, dm_result **out);
+
+/*
+ * Step-level entry points: the join program of Alg. 1 executed one
+ * step at a time on device rows, for drivers that move levels between ranks (§8(e)).
+ *   dm_plan_create_for: the plan dm_match would execute for (g, pattern, opt): the §3.3
+ *       decomposition plus the join order chosen with g's statistics; count_only planning when
+ *       !(opt->output & DM_OUT_TABLE).  Free with dm_plan_destroy.
+ *   dm_plan_width / dm_plan_stride: columns / int32 words per row of level `level` (the input of
+ *       step `level`; level num_steps is the final level, width k).  Level rows are row-major
+ *       int32 [rows][stride], stride = round_up(width, 4), padding -1, columns in plan (match)
+ *       order (dm_plan_column_vertex maps a column to its pattern vertex).
+ *   dm_plan_seed_work: HOST work_prefix[0..seed_end-seed_begin] = exclusive prefix of the seed
+ *       step's estimated work (deg(v)^n_new + 1) over the seed vertices v in [seed_begin,
+ *       seed_end) (seed_end < 0 means n).  dm_plan_seed_cuts: HOST cuts[0..parts] = equal-work
+ *       cut points of [0, n) over that prefix (rank r's seed range is [cuts[r], cuts[r+1])).
+ *   dm_plan_seed = dm_plan_step(step 0): the first slice's table (Alg. 1 l.2/l.6, reading Q3)
+ *       for opt's seed range, as a level.
+ *   dm_plan_step: run step `step` (0 <= step < num_steps) on the device rows d_in [in_rows]
+ *       of level `step` (step 0: d_in must be NULL, the seed range of opt is used).  Returns
+ *       level step+1 in *out_level (owned by the caller, dm_frontier_free; the final level's
+ *       work pointer is NULL) and its row count in *count when count != NULL.  For the last
+ *       step out_level may be NULL: then only *count (the count-only last step) is produced.
+ *   dm_plan_finish_table: final-level rows (plan order, stride round_up(k,4)) -> d_canon_out
+ *       [rows][k] in pattern-vertex column order and ascending lexicographic row order (a9).
+ *   dm_plan_run: dm_match with this plan.
+ * All run on opt->cuda_stream and return after the stream work they issued has completed.
+ * Errors: DM_ERR_ARG (NULL / ranges / a plan this graph cannot execute) plus dm_match's.
+ */
+DM_API dm_status dm_plan_create_for(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                                    const dm_match_opts *opt, dm_plan **out);
+DM_API int32_t dm_plan_width(const dm_plan *p, int32_t level);
+DM_API int32_t dm_plan_stride(const dm_plan *p, int32_t level);
+DM_API int32_t dm_plan_column_vertex(const dm_plan *p, int32_t column);
+DM_API dm_status dm_plan_seed_work(const dm_graph *g, const dm_plan *p, int64_t seed_begin,
+                                   int64_t seed_end, uint64_t *work_prefix);
+DM_API dm_status dm_plan_seed_cuts(const dm_graph *g, const dm_plan *p, int32_t parts, int64_t *cuts);
+DM_API dm_status dm_plan_seed(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt,
+                              dm_frontier **out);
+DM_API dm_status dm_plan_step(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt,
+                              int32_t step, const int32_t *d_in, int64_t in_rows,
+                              dm_frontier **out_level, uint64_t *count);
+DM_API dm_status dm_plan_finish_table(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt,
+                                      const int32_t *d_rows, int64_t rows, int32_t *d_canon_out);
+DM_API dm_status dm_plan_run(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt,
+                             dm_result **out);
+
+/*
+ * Multi-GPU exchange helpers (collectives C2 and C4).  Every row of a level is an
+ * independent candidate (§4.1), so any row partition is valid.  Device buffers on one
+ * device (the device of d_rows); stream-ordered on `stream` (cudaStream_t, NULL = legacy);
+ * the per-part row counts are written to the HOST array counts[parts] (the call synchronises).
+ *   dm_rows_partition_by_work: d_out = the n rows (stride int32 words each) grouped by
+ *       destination part, stable within a part; a row's part is floor(parts * (work_base + the
+ *       exclusive prefix of d_work at that row) / work_total) -- its position in the GLOBAL
+ *       work order of all ranks (work_base = total work of lower ranks), i.e. an equal-work cut.
+ *   dm_rows_partition_by_key: the same with part = #{splitters <= row[col]} (splitters: HOST
+ *       int32[parts-1], ascending): the range partition of a table by one column.
+ *   dm_table_sort: rows of d_rows [n][k] (packed) into ascending lexicographic order, in place
+ *       (ids in [0, n_vertices)).
+ * d_out must hold n * stride int32 and must not alias d_rows.
+ * Errors: DM_ERR_ARG (bad sizes, not device memory, unsorted splitters), DM_ERR_OOM, DM_ERR_CUDA.
+ */
+DM_API dm_status dm_rows_partition_by_work(const int32_t *d_rows, const uint64_t *d_work, int64_t n,
+                                           int32_t stride, uint64_t work_base, uint64_t work_total,
+                                           int32_t parts, int32_t *d_out, int64_t *counts, void *stream);
+DM_API dm_status dm_rows_partition_by_key(const int32_t *d_rows, int64_t n, int32_t stride, int32_t col,
+                                          const int32_t *splitters, int32_t parts, int32_t *d_out,
+                                          int64_t *counts, void *stream);
+DM_API dm_status dm_table_sort(int32_t *d_rows, int64_t n, int32_t k, int32_t n_vertices, void *stream);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 DM_API const char *dm_last_error(void);

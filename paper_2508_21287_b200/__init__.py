@@ -30,9 +30,9 @@ DM_OUT_COUNT, DM_OUT_TABLE = 1, 2
 DM_MOTIF_M2, DM_MOTIF_M3, DM_MOTIF_M3O = 1, 2, 4
 DM_GRAPH_DROP_SELF_LOOPS = 1
 DM_MATCH_PROFILE = 1
-DM_MAX_PATTERN = 64
-DM_MAX_STEPS = 64
-ABI_VERSION = 2
+DM_MAX_PATTERN = 128
+DM_MAX_STEPS = 128
+ABI_VERSION = 3
 
 MOTIF_SETS = {
     "all": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O,
@@ -65,6 +65,7 @@ class _Stats(ctypes.Structure):
                 ("width_in", ctypes.c_int32 * DM_MAX_STEPS),
                 ("width_out", ctypes.c_int32 * DM_MAX_STEPS),
                 ("bytes_model", ctypes.c_double * DM_MAX_STEPS),
+                ("bytes_stored", ctypes.c_double * DM_MAX_STEPS),
                 ("ms_count", ctypes.c_double * DM_MAX_STEPS),
                 ("ms_write", ctypes.c_double * DM_MAX_STEPS),
                 ("ms_other", ctypes.c_double), ("ms_total", ctypes.c_double),
@@ -82,7 +83,10 @@ EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_
            "dm_plan_num_slices", "dm_plan_slice", "dm_plan_num_steps", "dm_plan_first_vertex",
            "dm_plan_describe", "dm_match_prefix", "dm_frontier_rows", "dm_frontier_width",
            "dm_frontier_stride", "dm_frontier_device_rows", "dm_frontier_device_work",
-           "dm_frontier_free", "dm_match_resume"]
+           "dm_frontier_free", "dm_match_resume", "dm_frontier_work_total", "dm_plan_create_for",
+           "dm_plan_width", "dm_plan_stride", "dm_plan_column_vertex", "dm_plan_seed_work",
+           "dm_plan_seed_cuts", "dm_plan_seed", "dm_plan_step", "dm_plan_finish_table", "dm_plan_run",
+           "dm_rows_partition_by_work", "dm_rows_partition_by_key", "dm_table_sort"]
 
 
 def lib():
@@ -137,6 +141,23 @@ def lib():
         "dm_frontier_free": (None, [P]),
         "dm_match_resume": (c.c_int, [P, c.c_int32, P, c.c_int64, c.POINTER(_Opts), c.c_int32, P,
                                       c.c_int64, c.POINTER(P)]),
+        "dm_frontier_work_total": (c.c_uint64, [P]),
+        "dm_plan_create_for": (c.c_int, [P, c.c_int32, P, c.c_int64, c.POINTER(_Opts), c.POINTER(P)]),
+        "dm_plan_width": (c.c_int32, [P, c.c_int32]),
+        "dm_plan_stride": (c.c_int32, [P, c.c_int32]),
+        "dm_plan_column_vertex": (c.c_int32, [P, c.c_int32]),
+        "dm_plan_seed_work": (c.c_int, [P, P, c.c_int64, c.c_int64, P]),
+        "dm_plan_seed_cuts": (c.c_int, [P, P, c.c_int32, P]),
+        "dm_plan_seed": (c.c_int, [P, P, c.POINTER(_Opts), c.POINTER(P)]),
+        "dm_plan_step": (c.c_int, [P, P, c.POINTER(_Opts), c.c_int32, P, c.c_int64, c.POINTER(P),
+                                   c.POINTER(c.c_uint64)]),
+        "dm_plan_finish_table": (c.c_int, [P, P, c.POINTER(_Opts), P, c.c_int64, P]),
+        "dm_plan_run": (c.c_int, [P, P, c.POINTER(_Opts), c.POINTER(P)]),
+        "dm_rows_partition_by_work": (c.c_int, [P, P, c.c_int64, c.c_int32, c.c_uint64, c.c_uint64,
+                                                c.c_int32, P, P, P]),
+        "dm_rows_partition_by_key": (c.c_int, [P, c.c_int64, c.c_int32, c.c_int32, P, c.c_int32, P, P,
+                                               P]),
+        "dm_table_sort": (c.c_int, [P, c.c_int64, c.c_int32, c.c_int32, P]),
     }
     for name, (rt, args) in sig.items():
         f = getattr(L, name)
@@ -164,6 +185,68 @@ def _motifs(m) -> int:
     return int(m)
 
 
+def _check_rows(rows, graph, stride: int):
+    """Device rows handed to the library: int32, contiguous, on the graph's device, [n][stride]."""
+    import torch
+    if not isinstance(rows, torch.Tensor):
+        raise TypeError("rows must be a torch tensor")
+    if rows.dtype != torch.int32 or not rows.is_cuda or not rows.is_contiguous():
+        raise ValueError("rows must be a contiguous int32 CUDA tensor")
+    if graph is not None and rows.device.index != lib().dm_graph_device(graph._h):
+        raise ValueError("rows live on another device than the graph")
+    if rows.dim() != 2 or int(rows.shape[1]) != int(stride):
+        raise ValueError(f"rows must have shape [n, {stride}] (got {tuple(rows.shape)})")
+
+
+def _stream_ptr(stream):
+    if stream is None:
+        return None
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+# ------------------------------------------------------------------- exchange (§8(e))
+def partition_by_work(rows, work, work_base: int, work_total: int, parts: int, *, stream=None):
+    """dm_rows_partition_by_work: rows grouped by destination part (equal-work position in the
+    global work order); returns (packed CUDA tensor, per-part row counts)."""
+    import torch
+    _check_rows(rows, None, int(rows.shape[1]) if rows.dim() == 2 else -1)
+    n = int(rows.shape[0])
+    out = torch.empty_like(rows)
+    counts = np.zeros(int(parts), dtype=np.int64)
+    if n:
+        if work is None or work.dtype != torch.int64 or not work.is_cuda or work.shape != (n,):
+            raise ValueError("work must be an int64 CUDA tensor [n]")
+    _check(lib().dm_rows_partition_by_work(rows.data_ptr() if n else None, work.data_ptr() if n else None, n,
+                                           int(rows.shape[1]), int(work_base), int(work_total), int(parts),
+                                           out.data_ptr() if n else None, counts.ctypes.data, _stream_ptr(stream)))
+    return out, [int(c) for c in counts]
+
+
+def partition_by_key(rows, col: int, splitters, parts: int, *, stream=None):
+    """dm_rows_partition_by_key: rows grouped by the range of column `col` (range partition)."""
+    import torch
+    _check_rows(rows, None, int(rows.shape[1]) if rows.dim() == 2 else -1)
+    n = int(rows.shape[0])
+    out = torch.empty_like(rows)
+    sp = np.ascontiguousarray(np.asarray(splitters, dtype=np.int32).reshape(-1))
+    if sp.size != int(parts) - 1:
+        raise ValueError("need parts - 1 splitters")
+    counts = np.zeros(int(parts), dtype=np.int64)
+    _check(lib().dm_rows_partition_by_key(rows.data_ptr() if n else None, n, int(rows.shape[1]), int(col),
+                                          sp.ctypes.data if sp.size else None, int(parts),
+                                          out.data_ptr() if n else None, counts.ctypes.data, _stream_ptr(stream)))
+    return out, [int(c) for c in counts]
+
+
+def table_sort(rows, n_vertices: int, *, stream=None):
+    """dm_table_sort: lexicographic row order of a CUDA int32 [n][k] table, in place."""
+    _check_rows(rows, None, int(rows.shape[1]) if rows.dim() == 2 else -1)
+    n = int(rows.shape[0])
+    _check(lib().dm_table_sort(rows.data_ptr() if n else None, n, int(rows.shape[1]), int(n_vertices),
+                               _stream_ptr(stream)))
+    return rows
+
+
 # ------------------------------------------------------------------------------- plans
 class Plan:
     """Host join program (dm_plan_create): the §3.3 decomposition and the executed steps."""
@@ -186,10 +269,89 @@ class Plan:
                                        int(bool(stats.get("count_only", False))), ctypes.byref(h)))
         self._h = h
 
+    @classmethod
+    def for_graph(cls, graph: "Graph", k: int, p_edges, *, mode: str = "mono", output: str = "count",
+                  motifs="all") -> "Plan":
+        """dm_plan_create_for: the plan dm_match executes for (graph, pattern, options)."""
+        pe = _edges_arr(p_edges)
+        o = graph._opts(mode, output, motifs, None, None, False, 0, 0)
+        h = ctypes.c_void_p()
+        _check(lib().dm_plan_create_for(graph._h, int(k), pe.ctypes.data if pe.size else None,
+                                        pe.shape[0], ctypes.byref(o), ctypes.byref(h)))
+        self = cls.__new__(cls)
+        self._h = h
+        self.k = int(k)
+        self.mode, self.motifs = mode, motifs
+        return self
+
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.dm_plan_destroy(self._h)
             self._h = None
+
+    # ---- step-level execution (dm_plan_*; SURVEY §8(b))
+    def width(self, level: int) -> int:
+        return int(lib().dm_plan_width(self._h, int(level)))
+
+    def stride(self, level: int) -> int:
+        return int(lib().dm_plan_stride(self._h, int(level)))
+
+    def column_vertex(self, column: int) -> int:
+        return int(lib().dm_plan_column_vertex(self._h, int(column)))
+
+    def seed_work(self, graph: "Graph", seed_begin: int = 0, seed_end: int = -1) -> np.ndarray:
+        n = graph.n if seed_end < 0 else int(seed_end)
+        out = np.zeros(n - int(seed_begin) + 1, dtype=np.uint64)
+        _check(lib().dm_plan_seed_work(graph._h, self._h, int(seed_begin), int(seed_end), out.ctypes.data))
+        return out
+
+    def seed_cuts(self, graph: "Graph", parts: int) -> list:
+        out = np.zeros(int(parts) + 1, dtype=np.int64)
+        _check(lib().dm_plan_seed_cuts(graph._h, self._h, int(parts), out.ctypes.data))
+        return [int(x) for x in out]
+
+    def step(self, graph: "Graph", step: int, rows=None, *, seed_range=None, stream=None,
+             materialize: bool = True):
+        """dm_plan_step: level step+1 as a Frontier (materialize=True), or the count of the
+        count-only last step (materialize=False).  rows: CUDA int32 [n][stride(step)] tensor
+        (None for step 0: the implicit seed over seed_range)."""
+        o = graph._opts("mono", "count", "all", seed_range, stream, False, 0, 0)
+        ptr, n = None, 0
+        if rows is not None:
+            _check_rows(rows, graph, self.stride(step))
+            n = int(rows.shape[0])
+            ptr = rows.data_ptr() if n else None
+        cnt = ctypes.c_uint64(0)
+        if materialize:
+            h = ctypes.c_void_p()
+            _check(lib().dm_plan_step(graph._h, self._h, ctypes.byref(o), int(step), ptr, n, ctypes.byref(h),
+                                      ctypes.byref(cnt)))
+            return Frontier(h)
+        _check(lib().dm_plan_step(graph._h, self._h, ctypes.byref(o), int(step), ptr, n, None, ctypes.byref(cnt)))
+        return int(cnt.value)
+
+    def seed(self, graph: "Graph", *, seed_range=None, stream=None) -> "Frontier":
+        return self.step(graph, 0, None, seed_range=seed_range, stream=stream)
+
+    def finish_table(self, graph: "Graph", rows, *, stream=None):
+        """dm_plan_finish_table: final-level rows -> canonical CUDA tensor [n][k]."""
+        import torch
+        _check_rows(rows, graph, self.stride(self.num_steps))
+        n = int(rows.shape[0])
+        k = self.width(self.num_steps)
+        out = torch.empty((n, k), dtype=torch.int32, device=rows.device)
+        o = graph._opts("mono", "count", "all", None, stream, False, 0, 0)
+        _check(lib().dm_plan_finish_table(graph._h, self._h, ctypes.byref(o), rows.data_ptr() if n else None, n,
+                                          out.data_ptr() if n else None))
+        return out
+
+    def run(self, graph: "Graph", *, output: str = "count", seed_range=None, stream=None,
+            profile: bool = False) -> "Result":
+        """dm_plan_run: dm_match with this plan."""
+        o = graph._opts(getattr(self, "mode", "mono"), output, "all", seed_range, stream, profile, 0, 0)
+        r = ctypes.c_void_p()
+        _check(lib().dm_plan_run(graph._h, self._h, ctypes.byref(o), ctypes.byref(r)))
+        return graph._result(r, self.width(self.num_steps), output)
 
     @property
     def num_steps(self) -> int:
@@ -236,7 +398,8 @@ def _stats_dict(s: _Stats) -> dict:
         "rows_in": list(s.rows_in)[:n], "rows_out": list(s.rows_out)[:n],
         "candidates": list(s.candidates)[:n], "probes": list(s.probes)[:n],
         "width_in": list(s.width_in)[:n], "width_out": list(s.width_out)[:n],
-        "bytes_model": list(s.bytes_model)[:n], "ms_count": list(s.ms_count)[:n],
+        "bytes_model": list(s.bytes_model)[:n], "bytes_stored": list(s.bytes_stored)[:n],
+        "ms_count": list(s.ms_count)[:n],
         "ms_write": list(s.ms_write)[:n], "ms_other": s.ms_other, "ms_total": s.ms_total,
         "pipelined": bool(s.pipelined),
     }
@@ -262,6 +425,7 @@ class Frontier:
         self.rows = int(L.dm_frontier_rows(h))
         self.width = int(L.dm_frontier_width(h))
         self.stride = int(L.dm_frontier_stride(h))
+        self.work_total = int(L.dm_frontier_work_total(h))
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -275,8 +439,11 @@ class Frontier:
         return torch.as_tensor(_CudaArray(p, (self.rows, self.stride), "<i4", self), device=device)
 
     def work_tensor(self, device=None):
+        """torch view of the per-row work estimates (None for the final level)."""
         import torch
         p = lib().dm_frontier_device_work(self._h)
+        if not p:
+            return None
         return torch.as_tensor(_CudaArray(p, (self.rows,), "<i8", self), device=device)
 
 
@@ -312,6 +479,14 @@ class Graph:
     @property
     def max_degree(self) -> int:
         return lib().dm_graph_max_degree(self._h)
+
+    @property
+    def device(self) -> int:
+        return lib().dm_graph_device(self._h)
+
+    def plan(self, k: int, p_edges, **kw) -> Plan:
+        """dm_plan_create_for: the join program dm_match runs for this pattern."""
+        return Plan.for_graph(self, k, p_edges, **kw)
 
     def stats(self, count_only: bool = True) -> dict:
         """Cost-model statistics (for Plan(..., stats=g.stats()) == the plan dm_match uses)."""
@@ -359,6 +534,11 @@ class Graph:
         [rows][stride] (plan column order)."""
         pe = _edges_arr(p_edges)
         o = self._opts(mode, output, motifs, None, stream, profile, 0, 0)
+        if rows is not None:
+            plan = Plan.for_graph(self, k, pe, mode=mode, output=output, motifs=motifs)
+            if not 1 <= int(from_step) < plan.num_steps:
+                raise DMError(-1, "from_step must be in [1, num_steps)")
+            _check_rows(rows, self, plan.stride(from_step))
         n = int(rows.shape[0]) if rows is not None else 0
         ptr = rows.data_ptr() if n else None
         r = ctypes.c_void_p()

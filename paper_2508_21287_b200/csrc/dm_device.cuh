@@ -95,12 +95,25 @@ struct StepIO {
                               //   must be re-run), [2] += survivors / output reservation (zeroed)
   uint64_t cap;               // single pass: output capacity in rows
   const unsigned long long *d_in_rows;  // if set: the input row count, written on the device by
-                                        // the previous step (in_rows is then only an upper bound)
+                                        // the previous step (in_rows is then the capacity bound)
+  const unsigned long long *d_in_ovf;   // if set: the previous step's overflow flag (its ctrl[1]);
+                                        // non-zero -> the input level is incomplete, do nothing
   int32_t slots;              // row-serial kernel: survivor slots per row (set by launch)
   const int32_t *ell;         // row-serial kernel: ELL adjacency (max degree <= 4) or nullptr
   int32_t elem;               // bytes per stored vertex id in `in`: 4 (int32) or 2 (uint16)
   int32_t out_elem;           // bytes per stored vertex id in `out`
 };
+
+// Sync-free chaining: resolve the device-written input size.  Returns false when the previous
+// level overflowed its capacity (its rows are incomplete: the host re-runs the match on the
+// synchronising path); the size is clamped to the capacity the buffer was allocated with.
+__device__ __forceinline__ bool resolve_in_rows(StepIO &io) {
+  if (!io.d_in_rows) return true;
+  if (io.d_in_ovf && *io.d_in_ovf) return false;
+  const long long v = (long long)*io.d_in_rows;
+  io.in_rows = v < io.in_rows ? v : io.in_rows;
+  return true;
+}
 
 size_t step_smem_bytes(int in_w, bool write_pass);
 cudaError_t launch_step_count(const DevStep &st, const StepIO &io, const dm_graph &g,

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kStepThreads)
     k_step(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
   StepIO io = io_;  // device-written input size (sync-free chaining)
-  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
+  if (!resolve_in_rows(io)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typedef cub::BlockScan<long long, kStepThreads> ScanLL;
   typedef cub::BlockScan<int, kStepThreads> ScanI;
@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
     k_rows(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
            const int32_t *__restrict__ adj) {
   StepIO io = io_;  // device-written input size (sync-free chaining)
-  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
+  if (!resolve_in_rows(io)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   typedef cub::BlockScan<int, kStepThreads> ScanI;
   __shared__ typename ScanI::TempStorage tmp;

@@ -28,13 +28,16 @@
 #include <vector>
 
 #include "dm_device.cuh"
+#include "exchange.cuh"
 
 struct dm_frontier {
   int device = 0;
+  cudaStream_t s = nullptr;           // stream the buffers were allocated on (stream-ordered free)
   int32_t *rows = nullptr;            // device, [n][row_stride(w)]
   uint64_t n = 0;
   int32_t w = 0;
-  unsigned long long *work = nullptr;  // device, [n]
+  unsigned long long *work = nullptr;  // device, [n] (nullptr for the final level)
+  uint64_t work_total = 0;             // sum of work[0..n)
 };
 
 struct dm_result {
@@ -46,37 +49,6 @@ struct dm_result {
 
 namespace dm {
 namespace {
-
-__global__ void k_iota(uint32_t *p, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    p[i] = (uint32_t)i;
-}
-
-// keys[i] = table[perm[i]][col]   (table rows have stride k = row_stride(pattern size))
-__global__ void k_gather_col(const int32_t *__restrict__ table, int k, int col,
-                             const uint32_t *__restrict__ perm, uint32_t *__restrict__ keys,
-                             int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x)
-    keys[i] = (uint32_t)table[(int64_t)perm[i] * k + col];
-}
-
-// out[i][p] = table[perm[i]][pvert_col[p]]   (column permutation to pattern order)
-struct ColMap {
-  int32_t c[DM_MAX_PATTERN];
-};
-__global__ void k_gather_rows(const int32_t *__restrict__ table, int k, int ks, const ColMap cm,
-                              const uint32_t *__restrict__ perm, int32_t *__restrict__ out,
-                              int64_t n) {
-  const int64_t total = n * k;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i = t / k;
-    int p = (int)(t - i * k);
-    out[t] = table[(int64_t)perm[i] * ks + cm.c[p]];
-  }
-}
 
 int grid_for(int64_t work) {
   int64_t b = (work + 255) / 256;
@@ -503,7 +475,7 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
   CK(ctrl.alloc((size_t)3 * nsteps, c.s), "ctrl");
   CK(cudaMemsetAsync(ctrl.p, 0, sizeof(unsigned long long) * 3 * nsteps, c.s), "memset");
   int32_t *in = nullptr;
-  const unsigned long long *d_in = nullptr;
+  const unsigned long long *d_in = nullptr, *d_ovf = nullptr;
   for (int si = 0; si < nsteps; ++si) {
     const DevStep &D = c.dsteps[(size_t)si];
     const bool last = si == nsteps - 1;
@@ -512,6 +484,7 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
     io.in = in;
     io.in_rows = (int64_t)cap_in;
     io.d_in_rows = d_in;
+    io.d_in_ovf = d_ovf;
     io.seed_base = si == 0 ? seed_base : 0;
     io.elem = level_elem(c, si);
     io.out_elem = level_elem(c, si + 1);
@@ -551,6 +524,7 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
       }
       in = out;
       d_in = ctrl.p + 3 * si + 2;
+      d_ovf = ctrl.p + 3 * si + 1;
       cap_in = cap[(size_t)si];
     }
   }
@@ -576,46 +550,26 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
 }
 
 // Permute columns to pattern order and sort rows lexicographically (LSD radix sort over the
-// columns, last column first).  Writes host rows.
-dm_status canonicalize(Ctx &c, int32_t *host_out) {
+// columns, last column first).  Writes the device table `d_out` [n][k] (or,
+// with d_out == nullptr, the host rows).
+dm_status canonicalize(Ctx &c, int32_t *host_out, int32_t *d_out = nullptr) {
   const int k = c.plan->k;
   const int64_t n = (int64_t)c.res_rows;
   if (n == 0) return DM_OK;
-  if (n >= (int64_t)UINT32_MAX) return fail(DM_ERR_ROW_BUDGET, "table too large to sort");
-  int end_bit = 1;
-  while (end_bit < 32 && ((uint64_t)c.g->n >> end_bit) != 0) ++end_bit;
-  DevBuf<uint32_t> keys, keys2, perm, perm2;
-  CK(keys.alloc((size_t)n, c.s), "sort keys");
-  CK(keys2.alloc((size_t)n, c.s), "sort keys");
-  CK(perm.alloc((size_t)n, c.s), "sort perm");
-  CK(perm2.alloc((size_t)n, c.s), "sort perm");
   Prof::Ev e;
   c.prof.begin(0, 2, e);
-  k_iota<<<grid_for(n), 256, 0, c.s>>>(perm.p, n);
-  CK(cudaGetLastError(), "iota");
-  c.st.num_launches++;
-  cub::DoubleBuffer<uint32_t> dk(keys.p, keys2.p), dv(perm.p, perm2.p);
-  size_t tb = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, n, 0, end_bit, c.s), "sort");
-  DevBuf<unsigned char> tmp;
-  CK(tmp.alloc(tb, c.s), "sort temp");
-  for (int p = k - 1; p >= 0; --p) {
-    const int col = c.plan->pvert_col[(size_t)p];
-    k_gather_col<<<grid_for(n), 256, 0, c.s>>>(c.d_res, row_stride(k), col, dv.Current(), dk.Current(), n);
-    CK(cudaGetLastError(), "gather");
-    CK(cub::DeviceRadixSort::SortPairs(tmp.p, tb, dk, dv, n, 0, end_bit, c.s), "sort");
-    c.st.num_launches += 2;
-  }
-  ColMap cm{};
-  for (int p = 0; p < k; ++p) cm.c[p] = c.plan->pvert_col[(size_t)p];
   DevBuf<int32_t> outb;
-  CK(outb.alloc((size_t)n * k, c.s), "canonical table");
-  k_gather_rows<<<grid_for(n * k), 256, 0, c.s>>>(c.d_res, k, row_stride(k), cm, dv.Current(), outb.p, n);
-  CK(cudaGetLastError(), "gather rows");
-  c.st.num_launches++;
+  int32_t *dst = d_out;
+  if (!dst) {
+    CK(outb.alloc((size_t)n * k, c.s), "canonical table");
+    dst = outb.p;
+  }
+  dm_status st = lex_sort_rows(c.d_res, n, row_stride(k), c.plan->pvert_col.data(), k, id_bits(c.g->n), dst, c.s);
+  if (st != DM_OK) return st;
+  c.st.num_launches += 2 + 2 * k;
   c.prof.end(e);
-  CK(cudaMemcpyAsync(host_out, outb.p, sizeof(int32_t) * (size_t)n * k, cudaMemcpyDeviceToHost, c.s),
-     "D2H table");
+  if (host_out)
+    CK(cudaMemcpyAsync(host_out, dst, sizeof(int32_t) * (size_t)n * k, cudaMemcpyDeviceToHost, c.s), "D2H table");
   CK(cudaStreamSynchronize(c.s), "sync");
   return DM_OK;
 }
@@ -707,13 +661,38 @@ struct FrontierOut {
   uint64_t n = 0;
   int w = 0;
   unsigned long long *work = nullptr;
+  uint64_t work_total = 0;
 };
 
+// What one match_impl call executes (dm_match and the step-level entry points share it).
+struct RunSpec {
+  const Plan *plan = nullptr;     // execute this plan (dm_plan_* calls) instead of the cached one
+  int stop_at = -1;               // collect level stop_at in [1, num_steps] (num_steps = final)
+  FrontierOut *fout = nullptr;    //   ... into this
+  int from_step = 0;              // start at this step from device rows (0 = implicit seed)
+  const int32_t *from_rows = nullptr;
+  int64_t from_n = 0;
+  int32_t *d_canon = nullptr;     // table mode: canonical table to this device buffer [count][k]
+  bool no_host_table = false;     //   ... and not to the host
+};
+
+// A plan handed in through the ABI must be executable on this graph in this mode: 3-4 vertex
+// steps exist only as the count-only last step on ELL graphs (max degree <= 4).
+dm_status check_plan(const Plan &plan, const dm_graph *g, bool table) {
+  const int ns = (int)plan.steps.size();
+  for (int si = 0; si < ns; ++si) {
+    const Step &st = plan.steps[(size_t)si];
+    if (st.n_new < 1 || st.n_new > kMaxNew) return fail(DM_ERR_ARG, "plan: bad step");
+    if (st.n_new > 2 && !(si == ns - 1 && !table && g->d_ell))
+      return fail(DM_ERR_ARG, "plan has a 3-4 vertex step that only a count-only last step on a "
+                              "max-degree-4 graph can run (build it with dm_plan_create_for)");
+  }
+  return DM_OK;
+}
+
 dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
-                     const dm_match_opts *opt_in, dm_result **out, int stop_at = -1,
-                     FrontierOut *fout = nullptr, int from_step = 0,
-                     const int32_t *from_rows = nullptr, int64_t from_n = 0) {
-  if (!g || (!out && !fout)) return fail(DM_ERR_ARG, "graph/out is NULL");
+                     const dm_match_opts *opt_in, dm_result **out, const RunSpec &rs = RunSpec()) {
+  if (!g || (!out && !rs.fout)) return fail(DM_ERR_ARG, "graph/out is NULL");
   static const bool trace = std::getenv("DM_TRACE_HOST") != nullptr;  // debug: host phase times
   auto t_start = std::chrono::steady_clock::now();
   auto tr = [&](const char *what) {
@@ -725,16 +704,23 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   dm_match_opts_init(&opt);
   if (opt_in) opt = *opt_in;
   if (!(opt.output & (DM_OUT_COUNT | DM_OUT_TABLE))) return fail(DM_ERR_ARG, "output must request count and/or table");
-  Plan plan;
-  PlanStats pstats;
-  pstats.n = (double)std::max<int32_t>(g->n, 2);
-  pstats.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
-  pstats.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
-  pstats.closure = g->closure;
-  pstats.count_only = !(opt.output & DM_OUT_TABLE);
-  pstats.max_degree = g->max_deg;
-  dm_status stt = cached_plan(k, p_edges, pm, opt.motifs, opt.mode, pstats, plan);
-  if (stt != DM_OK) return stt;
+  Plan plan_local;
+  const Plan *pp = rs.plan;
+  dm_status stt = DM_OK;
+  if (!pp) {
+    PlanStats pstats;
+    pstats.n = (double)std::max<int32_t>(g->n, 2);
+    pstats.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
+    pstats.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
+    pstats.closure = g->closure;
+    pstats.count_only = !(opt.output & DM_OUT_TABLE);
+    pstats.max_degree = g->max_deg;
+    stt = cached_plan(k, p_edges, pm, opt.motifs, opt.mode, pstats, plan_local);
+    if (stt != DM_OK) return stt;
+    pp = &plan_local;
+  }
+  const Plan &plan = *pp;
+  k = plan.k;
   tr("plan");
   int64_t sb = std::max<int64_t>(0, opt.seed_begin);
   int64_t se = opt.seed_end < 0 ? g->n : std::min<int64_t>(opt.seed_end, g->n);
@@ -744,11 +730,23 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   if (!dgd.ok) return fail(DM_ERR_CUDA, "cudaSetDevice failed");
   configure_pool(g->device);
 
+  const int nst = (int)plan.steps.size();
+  const int stop_at = rs.stop_at, from_step = rs.from_step;
+  if (stop_at >= 0 && (stop_at < 1 || stop_at > nst || stop_at <= from_step))
+    return fail(DM_ERR_ARG, "upto_step must be in [max(1, from_step + 1), num_steps]");
+  if (from_step != 0 && (from_step < 1 || from_step >= nst || (rs.from_n > 0 && !rs.from_rows)))
+    return fail(DM_ERR_ARG, "from_step must be in [1, num_steps) with device rows");
+
   Ctx c;
   c.g = g;
   c.plan = &plan;
   c.s = (cudaStream_t)opt.cuda_stream;
-  c.table = (opt.output & DM_OUT_TABLE) != 0;
+  // collecting the final level materializes it (table path, rows in match order)
+  c.table = (opt.output & DM_OUT_TABLE) != 0 || stop_at == nst;
+  if (rs.plan) {
+    stt = check_plan(plan, g, c.table);
+    if (stt != DM_OK) return stt;
+  }
   c.row_budget = opt.row_budget ? opt.row_budget : (1ull << 27);
   std::memset(&c.st, 0, sizeof(c.st));
   c.st.num_steps = (int32_t)plan.steps.size();
@@ -776,12 +774,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   c.prof.s = c.s;
   tr("setup+meminfo");
 
-  const int nst = (int)plan.steps.size();
-  if (stop_at >= 0 && (stop_at < 1 || stop_at >= nst))
-    return fail(DM_ERR_ARG, "upto_step must be in [1, num_steps)");
-  if (from_step != 0 && (from_step < 1 || from_step >= nst || (from_n > 0 && !from_rows)))
-    return fail(DM_ERR_ARG, "from_step must be in [1, num_steps) with device rows");
-  c.stop_at = stop_at;
+  c.stop_at = stop_at < nst ? stop_at : -1;  // the final level is collected from the result table
   // 16-bit frontier storage: count-only plans on max-degree-4 graphs with 16-bit vertex ids
   // (every step then runs in the row-serial kernels); not for tables or exchanged levels.
   if (!c.table && stop_at < 0 && from_step == 0 && g->d_ell && g->n <= 65535) c.elem = 2;
@@ -806,6 +799,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     ~AccGuard() {
       if (c.d_acc) cudaFreeAsync(c.d_acc, c.s);
       if (c.d_res) cudaFreeAsync(c.d_res, c.s);
+      if (c.d_front) cudaFreeAsync(c.d_front, c.s);
     }
   } ag{c};
   CK(cudaMemsetAsync(c.d_acc, 0, sizeof(unsigned long long) * nacc, c.s), "memset");
@@ -818,7 +812,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   uint64_t count = 0;
   if (plan.steps.empty()) {  // k == 1: every data vertex of the shard (Q7)
     count = (uint64_t)(se - sb);
-    if (c.table) {
+    if (c.table && !rs.no_host_table) {
       if (count > c.row_budget) return fail(DM_ERR_ROW_BUDGET, "result table exceeds row_budget");
       res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count, 1));
       if (!res->rows) return fail(DM_ERR_OOM, "host allocation failed");
@@ -831,7 +825,8 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     std::snprintf(kb, sizeof(kb), "%llu|%d|%d|%d|%lld|%lld|%d|", (unsigned long long)g->gen, k,
                   opt.mode, opt.motifs, (long long)sb, (long long)se, c.elem);
     std::string rkey(kb);
-    if (pm > 0) rkey.append(reinterpret_cast<const char *>(p_edges), (size_t)pm * 2 * sizeof(int32_t));
+    if (pm > 0 && p_edges) rkey.append(reinterpret_cast<const char *>(p_edges), (size_t)pm * 2 * sizeof(int32_t));
+    if (rs.plan) rkey += plan.describe();
     bool done = false;
     if (from_step == 0 && async_eligible(c)) {
       std::vector<double> rat;
@@ -841,7 +836,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
         auto it = rc.m.find(rkey);
         if (it != rc.m.end()) rat = it->second;
       }
-      if (!rat.empty()) {
+      if (rat.size() == plan.steps.size()) {
         stt = run_async(c, rat, se - sb, sb, done);
         if (stt != DM_OK) return stt;
         if (!done) {  // fall back: clear the partial counters and statistics
@@ -853,39 +848,66 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
       }
     }
     if (!done) {
-      if (from_step > 0) stt = run_step(c, from_step, from_rows, from_n, 0);
+      if (from_step > 0) stt = run_step(c, from_step, rs.from_rows, rs.from_n, 0);
       else stt = run_step(c, 0, nullptr, se - sb, sb);
     }
     if (stt == DM_OK && from_step == 0 && async_eligible(c)) {
+      // growth ratio of every level over the whole run (a chunked run's per-chunk ratios differ)
+      std::vector<double> rat(plan.steps.size(), 0.0);
+      for (int i = 0; i + 1 < nst; ++i)
+        rat[(size_t)i] = c.st.rows_in[i] ? (double)c.st.rows_out[i] / (double)c.st.rows_in[i] : 0.0;
       RatioCache &rc = ratio_cache();
       std::lock_guard<std::mutex> lk(rc.mu);
       if (rc.m.size() > 4096) rc.m.clear();
-      rc.m[rkey] = c.ratio;
+      rc.m[rkey] = rat;
     }
     tr("steps");
-    if (stt != DM_OK) {
-      if (c.d_front) cudaFreeAsync(c.d_front, c.s);
-      return stt;
-    }
-    if (stop_at >= 0) {  // dm_match_prefix: hand the collected level over with work estimates
-      fout->rows = c.d_front;
-      fout->n = c.front_rows;
-      fout->w = plan.steps[(size_t)stop_at].in_w;
-      CK(cudaMallocAsync((void **)&fout->work, sizeof(unsigned long long) * std::max<uint64_t>(c.front_rows, 1), c.s),
-         "work allocation");
-      if (c.front_rows) {
-        k_row_work<<<grid_for((int64_t)c.front_rows), 256, 0, c.s>>>(
-            c.d_front, (int64_t)c.front_rows, row_stride(fout->w), c.dsteps[(size_t)stop_at], g->d_off, fout->work);
-        CK(cudaGetLastError(), "work kernel");
+    if (stt != DM_OK) return stt;
+    if (stop_at >= 0) {  // step-level entry points: hand the collected level over
+      FrontierOut &fo = *rs.fout;
+      if (stop_at < nst) {
+        fo.rows = c.d_front;
+        fo.n = c.front_rows;
+        c.d_front = nullptr;
+        fo.w = plan.steps[(size_t)stop_at].in_w;
+        CK(cudaMallocAsync((void **)&fo.work, sizeof(unsigned long long) * std::max<uint64_t>(fo.n, 1), c.s),
+           "work allocation");
+        if (fo.n) {
+          k_row_work<<<grid_for((int64_t)fo.n), 256, 0, c.s>>>(fo.rows, (int64_t)fo.n, row_stride(fo.w),
+                                                                c.dsteps[(size_t)stop_at], g->d_off, fo.work);
+          CK(cudaGetLastError(), "work kernel");
+          unsigned long long *tot = nullptr;
+          CK(cudaMallocAsync((void **)&tot, sizeof(unsigned long long), c.s), "work total");
+          size_t tb = 0;
+          CK(cub::DeviceReduce::Sum(nullptr, tb, fo.work, tot, (int64_t)fo.n, c.s), "work total");
+          void *tmp = nullptr;
+          CK(cudaMallocAsync(&tmp, tb, c.s), "work total");
+          CK(cub::DeviceReduce::Sum(tmp, tb, fo.work, tot, (int64_t)fo.n, c.s), "work total");
+          unsigned long long *h = pinned_scratch();
+          CK(cudaMemcpyAsync(h, tot, sizeof(unsigned long long), cudaMemcpyDeviceToHost, c.s), "D2H work total");
+          cudaFreeAsync(tmp, c.s);
+          cudaFreeAsync(tot, c.s);
+          CK(cudaStreamSynchronize(c.s), "sync");
+          fo.work_total = h[0];
+        }
+      } else {  // the final level (plan column order, stride row_stride(k)); no next-step work
+        fo.rows = c.d_res;
+        fo.n = c.res_rows;
+        c.d_res = nullptr;
+        fo.w = k;
+        fo.work = nullptr;
+        fo.work_total = 0;
       }
       CK(cudaStreamSynchronize(c.s), "sync");
       return DM_OK;
     }
     if (c.table) {
       count = c.res_rows;
-      res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count * k, 1));
-      if (!res->rows) return fail(DM_ERR_OOM, "host allocation failed");
-      stt = canonicalize(c, res->rows);
+      if (!rs.no_host_table) {
+        res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count * k, 1));
+        if (!res->rows) return fail(DM_ERR_OOM, "host allocation failed");
+      }
+      stt = canonicalize(c, rs.no_host_table ? nullptr : res->rows, rs.d_canon);
       if (stt != DM_OK) return stt;
     }
   }
@@ -906,11 +928,15 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     c.st.candidates[i] = slot_sum(kAccSlots + 2 * kAccSlots * i);
     c.st.probes[i] = slot_sum(2 * kAccSlots + 2 * kAccSlots * i);
     const bool lastc = (i + 1 == plan.steps.size()) && !c.table;
-    const double win = (i == 0) ? 0.0 : (double)c.st.width_in[i];  // the seed input is implicit
+    const double rin = (double)c.st.rows_in[i], rout = (double)c.st.rows_out[i];
+    const double lookups = 8.0 * rin + 4.0 * (double)c.st.candidates[i] + 4.0 * (double)c.st.probes[i];
+    // SURVEY §8(d) as written: 4 B per id, the seed's one-column input included
+    c.st.bytes_model[i] = 4.0 * (double)c.st.width_in[i] * rin + lookups +
+                          (lastc ? 0.0 : 4.0 * (double)c.st.width_out[i] * rout);
+    // the same with the stored id width (2 B for 16-bit levels) and no read for the implicit seed
+    const double win = (i == 0 && from_step == 0) ? 0.0 : (double)c.st.width_in[i];
     const double ebi = (double)level_elem(c, (int)i), ebo = (double)level_elem(c, (int)i + 1);
-    c.st.bytes_model[i] = ebi * win * (double)c.st.rows_in[i] + 8.0 * (double)c.st.rows_in[i] +
-                          4.0 * (double)c.st.candidates[i] + 4.0 * (double)c.st.probes[i] +
-                          (lastc ? 0.0 : ebo * c.st.width_out[i] * (double)c.st.rows_out[i]);
+    c.st.bytes_stored[i] = ebi * win * rin + lookups + (lastc ? 0.0 : ebo * c.st.width_out[i] * rout);
   }
   res->count = count;
   c.st.elem_bytes = c.elem;  // bytes per stored vertex id in the frontier levels
@@ -918,6 +944,47 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   tr("done");
   rg.keep = true;
   *out = res;
+  return DM_OK;
+}
+
+dm_status make_frontier(const dm_graph *g, const dm_match_opts *opt, const FrontierOut &fo, dm_frontier **out) {
+  dm_frontier *f = new (std::nothrow) dm_frontier;
+  if (!f) {
+    DeviceGuard dg(g->device);
+    cudaStream_t s = opt ? (cudaStream_t)opt->cuda_stream : nullptr;
+    if (fo.rows) cudaFreeAsync(fo.rows, s);
+    if (fo.work) cudaFreeAsync(fo.work, s);
+    return fail(DM_ERR_OOM, "host allocation failed");
+  }
+  f->device = g->device;
+  f->s = opt ? (cudaStream_t)opt->cuda_stream : nullptr;
+  f->rows = fo.rows;
+  f->n = fo.n;
+  f->w = fo.w;
+  f->work = fo.work;
+  f->work_total = fo.work_total;
+  *out = f;
+  return DM_OK;
+}
+
+// Equal-work cut points over the seed vertices [0, n): work of seed v = (deg(v)+1)^n_new of the
+// plan's first step (the seed step's candidate count, the same estimate k_row_work uses).
+dm_status seed_work_prefix(const dm_graph *g, const Plan &plan, int64_t sb, int64_t se, std::vector<uint64_t> &wp) {
+  const int64_t n = g->n;
+  std::vector<int64_t> off((size_t)n + 1, 0);
+  if (n > 0) {
+    DeviceGuard dg(g->device);
+    if (!dg.ok) return fail(DM_ERR_CUDA, "cudaSetDevice failed");
+    CK(cudaMemcpy(off.data(), g->d_off, sizeof(int64_t) * ((size_t)n + 1), cudaMemcpyDeviceToHost), "D2H offsets");
+  }
+  const int nn = plan.steps.empty() ? 0 : plan.steps[0].n_new;
+  wp.assign((size_t)(se - sb) + 1, 0);
+  for (int64_t v = sb; v < se; ++v) {
+    const uint64_t d = (uint64_t)(off[(size_t)v + 1] - off[(size_t)v]);
+    uint64_t w = 1;
+    for (int j = 0; j < nn; ++j) w *= d;  // candidates of the seed step (deg, deg^2 for wedges)
+    wp[(size_t)(v - sb) + 1] = wp[(size_t)(v - sb)] + w + 1;  // +1: every seed costs a row
+  }
   return DM_OK;
 }
 
@@ -937,17 +1004,30 @@ dm_status dm_match_prefix(const dm_graph *g, int32_t k, const int32_t *p_edges, 
   dm::clear_error();
   if (!g || !out) return dm::fail(DM_ERR_ARG, "graph/out is NULL");
   dm::FrontierOut fo;
-  dm_status st = dm::match_impl(g, k, p_edges, pm, opt, nullptr, upto_step, &fo);
+  dm::RunSpec rs;
+  rs.stop_at = upto_step < 1 ? 0 : upto_step;
+  rs.fout = &fo;
+  // the prefix entry point never collects the final level (that is a table: use dm_match)
+  dm_match_opts o;
+  dm_match_opts_init(&o);
+  if (opt) o = *opt;
+  dm::Plan probe;
+  {
+    dm::PlanStats ps;
+    ps.n = (double)std::max<int32_t>(g->n, 2);
+    ps.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
+    ps.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
+    ps.closure = g->closure;
+    ps.count_only = !(o.output & DM_OUT_TABLE);
+    ps.max_degree = g->max_deg;
+    dm_status st = dm::cached_plan(k, p_edges, pm, o.motifs, o.mode, ps, probe);
+    if (st != DM_OK) return st;
+  }
+  if (upto_step < 1 || upto_step >= (int32_t)probe.steps.size())
+    return dm::fail(DM_ERR_ARG, "upto_step must be in [1, num_steps)");
+  dm_status st = dm::match_impl(g, k, p_edges, pm, &o, nullptr, rs);
   if (st != DM_OK) return st;
-  dm_frontier *f = new (std::nothrow) dm_frontier;
-  if (!f) return dm::fail(DM_ERR_OOM, "host allocation failed");
-  f->device = g->device;
-  f->rows = fo.rows;
-  f->n = fo.n;
-  f->w = fo.w;
-  f->work = fo.work;
-  *out = f;
-  return DM_OK;
+  return dm::make_frontier(g, &o, fo, out);
 }
 
 int64_t dm_frontier_rows(const dm_frontier *f) { return f ? (int64_t)f->n : -1; }
@@ -957,13 +1037,14 @@ const int32_t *dm_frontier_device_rows(const dm_frontier *f) { return f ? f->row
 const uint64_t *dm_frontier_device_work(const dm_frontier *f) {
   return f ? reinterpret_cast<const uint64_t *>(f->work) : nullptr;
 }
+uint64_t dm_frontier_work_total(const dm_frontier *f) { return f ? f->work_total : 0; }
 
 void dm_frontier_free(dm_frontier *f) {
   if (!f) return;
   dm::DeviceGuard dg(f->device);
-  cudaDeviceSynchronize();
-  if (f->rows) cudaFree(f->rows);
-  if (f->work) cudaFree(f->work);
+  // stream-ordered: after the work already enqueued on the frontier's stream (no device sync)
+  if (f->rows) cudaFreeAsync(f->rows, f->s);
+  if (f->work) cudaFreeAsync(f->work, f->s);
   delete f;
 }
 
@@ -972,7 +1053,132 @@ dm_status dm_match_resume(const dm_graph *g, int32_t k, const int32_t *p_edges, 
                           int64_t rows, dm_result **out) {
   dm::clear_error();
   if (rows < 0) return dm::fail(DM_ERR_ARG, "rows < 0");
-  return dm::match_impl(g, k, p_edges, pm, opt, out, -1, nullptr, from_step, d_rows, rows);
+  dm::RunSpec rs;
+  rs.from_step = from_step;
+  rs.from_rows = d_rows;
+  rs.from_n = rows;
+  return dm::match_impl(g, k, p_edges, pm, opt, out, rs);
+}
+
+// ------------------------------------------------------------------ step-level entry points
+dm_status dm_plan_create_for(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                             const dm_match_opts *opt, dm_plan **out) {
+  dm::clear_error();
+  if (!g || !out) return dm::fail(DM_ERR_ARG, "graph/out is NULL");
+  dm_match_opts o;
+  dm_match_opts_init(&o);
+  if (opt) o = *opt;
+  dm::PlanStats ps;
+  ps.n = (double)std::max<int32_t>(g->n, 2);
+  ps.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
+  ps.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
+  ps.closure = g->closure;
+  ps.count_only = !(o.output & DM_OUT_TABLE);
+  ps.max_degree = g->max_deg;
+  dm_plan *p = new (std::nothrow) dm_plan;
+  if (!p) return dm::fail(DM_ERR_OOM, "host allocation failed");
+  dm_status st = dm::cached_plan(k, p_edges, pm, o.motifs, o.mode, ps, p->p);
+  if (st != DM_OK) {
+    delete p;
+    return st;
+  }
+  *out = p;
+  return DM_OK;
+}
+
+dm_status dm_plan_seed_work(const dm_graph *g, const dm_plan *p, int64_t seed_begin, int64_t seed_end,
+                            uint64_t *work_prefix) {
+  dm::clear_error();
+  if (!g || !p || !work_prefix) return dm::fail(DM_ERR_ARG, "NULL argument");
+  if (seed_end < 0) seed_end = g->n;
+  if (seed_begin < 0 || seed_begin > seed_end || seed_end > g->n) return dm::fail(DM_ERR_ARG, "bad seed range");
+  std::vector<uint64_t> wp;
+  dm_status st = dm::seed_work_prefix(g, p->p, seed_begin, seed_end, wp);
+  if (st != DM_OK) return st;
+  std::memcpy(work_prefix, wp.data(), sizeof(uint64_t) * wp.size());
+  return DM_OK;
+}
+
+dm_status dm_plan_seed_cuts(const dm_graph *g, const dm_plan *p, int32_t parts, int64_t *cuts) {
+  dm::clear_error();
+  if (!g || !p || !cuts || parts < 1) return dm::fail(DM_ERR_ARG, "bad argument");
+  std::vector<uint64_t> wp;
+  dm_status st = dm::seed_work_prefix(g, p->p, 0, g->n, wp);
+  if (st != DM_OK) return st;
+  const uint64_t total = wp.back();
+  cuts[0] = 0;
+  for (int r = 1; r < parts; ++r) {
+    const uint64_t target = (uint64_t)(((unsigned __int128)total * (unsigned)r) / (unsigned)parts);
+    const int64_t v = (int64_t)(std::lower_bound(wp.begin(), wp.end(), target) - wp.begin());
+    cuts[r] = std::min<int64_t>(std::max<int64_t>(v, cuts[r - 1]), g->n);
+  }
+  cuts[parts] = g->n;
+  return DM_OK;
+}
+
+dm_status dm_plan_step(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt, int32_t step,
+                       const int32_t *d_in, int64_t in_rows, dm_frontier **out_level, uint64_t *count) {
+  dm::clear_error();
+  if (!g || !p || (!out_level && !count)) return dm::fail(DM_ERR_ARG, "NULL argument");
+  const int nst = (int)p->p.steps.size();
+  if (step < 0 || step >= nst) return dm::fail(DM_ERR_ARG, "step out of range");
+  if (step > 0 && (in_rows < 0 || (in_rows > 0 && !d_in))) return dm::fail(DM_ERR_ARG, "bad input rows");
+  if (step == 0 && d_in) return dm::fail(DM_ERR_ARG, "step 0 reads the implicit seed (d_in must be NULL)");
+  if (!out_level && step + 1 < nst) return dm::fail(DM_ERR_ARG, "only the last step can count without output");
+  dm_match_opts o;
+  dm_match_opts_init(&o);
+  if (opt) o = *opt;
+  dm::RunSpec rs;
+  rs.plan = &p->p;
+  rs.from_step = step;
+  rs.from_rows = d_in;
+  rs.from_n = in_rows;
+  if (!out_level) {  // the count-only last step
+    o.output = DM_OUT_COUNT;
+    dm_result *r = nullptr;
+    dm_status st = dm::match_impl(g, p->p.k, nullptr, 0, &o, &r, rs);
+    if (st != DM_OK) return st;
+    *count = r->count;
+    dm_result_free(r);
+    return DM_OK;
+  }
+  dm::FrontierOut fo;
+  rs.stop_at = step + 1;
+  rs.fout = &fo;
+  if (step + 1 < nst) o.output = DM_OUT_COUNT;  // intermediate levels are never tables
+  dm_status st = dm::match_impl(g, p->p.k, nullptr, 0, &o, nullptr, rs);
+  if (st != DM_OK) return st;
+  if (count) *count = fo.n;
+  return dm::make_frontier(g, &o, fo, out_level);
+}
+
+dm_status dm_plan_seed(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt, dm_frontier **out) {
+  return dm_plan_step(g, p, opt, 0, nullptr, 0, out, nullptr);
+}
+
+dm_status dm_plan_run(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt, dm_result **out) {
+  dm::clear_error();
+  if (!g || !p || !out) return dm::fail(DM_ERR_ARG, "NULL argument");
+  dm::RunSpec rs;
+  rs.plan = &p->p;
+  return dm::match_impl(g, p->p.k, nullptr, 0, opt, out, rs);
+}
+
+dm_status dm_plan_finish_table(const dm_graph *g, const dm_plan *p, const dm_match_opts *opt, const int32_t *d_rows,
+                               int64_t rows, int32_t *d_canon_out) {
+  dm::clear_error();
+  if (!g || !p || rows < 0 || (rows > 0 && (!d_rows || !d_canon_out))) return dm::fail(DM_ERR_ARG, "bad argument");
+  if (rows == 0) return DM_OK;
+  const dm::Plan &pl = p->p;
+  dm::DeviceGuard dg(g->device);
+  if (!dg.ok) return dm::fail(DM_ERR_CUDA, "cudaSetDevice failed");
+  cudaStream_t s = opt ? (cudaStream_t)opt->cuda_stream : nullptr;
+  dm_status st = dm::lex_sort_rows(d_rows, rows, dm::row_stride(pl.k), pl.pvert_col.data(), pl.k,
+                                   dm::id_bits(g->n), d_canon_out, s);
+  if (st != DM_OK) return st;
+  cudaError_t e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return dm::fail(DM_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  return DM_OK;
 }
 
 uint64_t dm_result_count(const dm_result *r) { return r ? r->count : 0; }

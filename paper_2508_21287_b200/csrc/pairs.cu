@@ -22,9 +22,9 @@ __global__ void __launch_bounds__(kStepThreads)
             const int32_t *__restrict__ adj, int32_t *__restrict__ slab, int64_t slab_cap,
             int pair_mode, unsigned long long *__restrict__ row_counter) {
   StepIO io = io_;  // device-written input size (sync-free chaining)
-  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
+  if (!resolve_in_rows(io)) return;
   constexpr int kWarps = kStepThreads / 32;
-  __shared__ __align__(16) int32_t s_row[kWarps][64];
+  __shared__ __align__(16) int32_t s_row[kWarps][DM_MAX_PATTERN];
   __shared__ int32_t s_list[kWarps][kPairSmem];
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t wg = (int64_t)blockIdx.x * kWarps + wl;

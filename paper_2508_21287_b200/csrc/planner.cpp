@@ -439,6 +439,23 @@ dm_status dm_plan_slice(const dm_plan *p, int32_t i, int32_t *motif, int32_t *n_
 int32_t dm_plan_num_steps(const dm_plan *p) { return p ? (int32_t)p->p.steps.size() : -1; }
 int32_t dm_plan_first_vertex(const dm_plan *p) { return p ? p->p.first_vertex : -1; }
 
+int32_t dm_plan_width(const dm_plan *p, int32_t level) {
+  if (!p) return -1;
+  const int ns = (int)p->p.steps.size();
+  if (level < 0 || level > ns) return -1;
+  return level == ns ? p->p.k : p->p.steps[(size_t)level].in_w;
+}
+
+int32_t dm_plan_stride(const dm_plan *p, int32_t level) {
+  const int32_t w = dm_plan_width(p, level);
+  return w < 0 ? -1 : ((w + 3) & ~3);
+}
+
+int32_t dm_plan_column_vertex(const dm_plan *p, int32_t column) {
+  if (!p || column < 0 || column >= (int32_t)p->p.col_pvert.size()) return -1;
+  return p->p.col_pvert[(size_t)column];
+}
+
 int64_t dm_plan_describe(const dm_plan *p, char *buf, int64_t len) {
   if (!p) return -1;
   std::string s = p->p.describe();

@@ -118,13 +118,14 @@ __device__ __forceinline__ unsigned dfs_ell(const DevStep &st, const int32_t *ro
 // threads, each finishing x_2, x_3 of its entries.  The per-row 4-deep recursion left 17 of 32
 // lanes idle (rows' subtrees differ); the queue rebalances the second half within the tile.
 constexpr int kTailQueuePerRow = 4;
+static_assert(kTileRows <= 256, "TailQueue stores the row of an entry in a uint8");
 
 template <int NQ>
 __global__ void __launch_bounds__(kStepThreads, 4)
     k_deep_split(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
                  const int32_t *__restrict__ adj) {
   StepIO io = io_;  // device-written input size (sync-free chaining)
-  if (io.d_in_rows) io.in_rows = (int64_t)*io.d_in_rows;
+  if (!resolve_in_rows(io)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t s_bar;
   __shared__ int s_qn;
@@ -201,14 +202,19 @@ cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, 
   // Shared memory only for the register-limited number of resident CTAs; the rest of the
   // unified array stays L1 for the ELL lists (160 KB on heavy-hex w=31): with the maximal
   // carveout the ELL loads hit L1 70% of the time, the tile rows need only ~120 KB per SM.
-  static std::mutex mu;
-  static std::map<const void *, int> carve;
-  int cv = 100;
+  // Configured per (device, kernel) whenever a launch needs more dynamic shared memory than
+  // the kernel was configured for (k_deep_split<0> serves every row width > 32 columns).
   {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> configured;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lk(mu);
-    auto it = carve.find((const void *)kern);
-    if (it == carve.end()) {
-      cudaError_t e = prep((const void *)kern, 0, smem);
+    const auto key = std::make_pair(dev, (const void *)kern);
+    auto it = configured.find(key);
+    if (it == configured.end() || it->second < smem) {
+      e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       int nb = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kStepThreads, smem);
@@ -217,11 +223,11 @@ cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, 
       e = cudaFuncGetAttributes(&fa, (const void *)kern);
       if (e != cudaSuccess) return e;
       const double need = (double)nb * (double)(smem + fa.sharedSizeBytes + 1024);
-      cv = (int)std::ceil(100.0 * need / (228.0 * 1024.0));
+      int cv = (int)std::ceil(100.0 * need / (228.0 * 1024.0));
       cv = cv < 1 ? 1 : (cv > 100 ? 100 : cv);
       e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributePreferredSharedMemoryCarveout, cv);
       if (e != cudaSuccess) return e;
-      carve[(const void *)kern] = cv;
+      configured[key] = smem;
     }
   }
   kern<<<(unsigned)tiles, kStepThreads, smem, s>>>(st, io2, g.d_off, g.d_adj);

@@ -166,8 +166,10 @@ def test_plan_errors(dm):
         dm.Plan(3, [(0, 5)])
     assert ei.value.code == -2
     with pytest.raises(dm.DMError) as ei:
-        dm.Plan(65, [(i, i + 1) for i in range(64)])
+        dm.Plan(129, [(i, i + 1) for i in range(128)])
     assert ei.value.code == -8
+    P = dm.Plan(100, [(i, i + 1) for i in range(99)])   # the paper's Table 2 sizes go to 100
+    assert P.width(P.num_steps) == 100 and P.num_steps <= dm.DM_MAX_STEPS
     P = dm.Plan(1, np.zeros((0, 2), np.int32))
     assert P.num_steps == 0 and P.first_vertex == 0
 

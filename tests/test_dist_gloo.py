@@ -1,7 +1,12 @@
-"""Multi-rank host logic on CPU (gloo, world_size 2): equal-work seed cuts, the count
-all_reduce (C3) and the table gather + canonical merge (C4).  The per-rank matcher is the
-oracle restricted to the rank's root range, so the test checks that the sharding partitions
-the result exactly (SURVEY §8(e) invariant: 1/2/4/8-rank results are identical)."""
+"""Multi-rank collective sequencing on CPU (gloo, world_size 2 and 3): the frontier rebalance
+(C1 all_gather of work totals + C2 all_to_all of rows), the count all_reduce (C3) and the range
+partition + exchange + sort of the canonical table (C4) of paper_2508_21287_b200.dist.
+
+dist.py takes its device operations (the library's partition / sort kernels) as parameters; here
+they are replaced by plain CPU definitions written in this file, so the test checks the
+collective plumbing and the SURVEY §8(e) invariants (rows conserved, every rank ~1/world of the
+work, sharded results identical to the unsharded oracle).  The same functions run with the
+library kernels on the GPU in tests/test_gpu_dist.py."""
 import os
 import socket
 
@@ -10,7 +15,6 @@ import pytest
 import torch.multiprocessing as mp
 
 import dm_inputs as g
-from paper_2508_21287_b200.dist import equal_work_cuts, match_sharded, merge_tables
 
 
 def _free_port():
@@ -21,79 +25,107 @@ def _free_port():
     return p
 
 
-def test_equal_work_cuts():
-    wp = np.cumsum([0] + [3] * 10)
-    assert equal_work_cuts(wp, 1) == [0, 10]
-    c = equal_work_cuts(wp, 2)
-    assert c[0] == 0 and c[-1] == 10 and c == sorted(c)
-    assert equal_work_cuts(np.array([0, 0, 0]), 4) == [0, 0, 0, 0, 2]
-    wp = np.cumsum([0, 100, 1, 1, 1, 1])
-    c = equal_work_cuts(wp, 3)
-    assert c[0] == 0 and c[-1] == 5 and all(a <= b for a, b in zip(c, c[1:]))
+# ---- CPU definitions of the library's device operations (test-side reference) -------------
+def cpu_partition_by_work(rows, work, base, total, parts, stream=None):
+    import torch
+    n = int(rows.shape[0])
+    if n == 0:
+        return rows.clone(), [0] * parts
+    excl = torch.cumsum(work, 0) - work
+    dest = [min(parts - 1, ((base + int(e)) * parts) // total) if total else 0 for e in excl.tolist()]
+    order = sorted(range(n), key=lambda i: dest[i])          # stable
+    counts = [dest.count(r) for r in range(parts)]
+    return rows[order].contiguous(), counts
 
 
-def _worker(rank, world, port, out):
+def cpu_partition_by_key(rows, col, splitters, parts, stream=None):
+    n = int(rows.shape[0])
+    if n == 0:
+        return rows.clone(), [0] * parts
+    dest = [int(np.searchsorted(np.asarray(splitters, np.int64), int(v), side="right"))
+            for v in rows[:, col].tolist()]
+    order = sorted(range(n), key=lambda i: dest[i])
+    return rows[order].contiguous(), [dest.count(r) for r in range(parts)]
+
+
+def cpu_sort(rows, n_vertices, stream=None):
+    import torch
+    a = rows.numpy()
+    if a.shape[0] == 0:
+        return rows
+    return torch.from_numpy(np.ascontiguousarray(a[np.lexsort(a.T[::-1])]))
+
+
+def _spawn(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q, *args)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    return res
+
+
+def _init(rank, world, port):
     import torch.distributed as tdist
-
-    import oracle
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     tdist.init_process_group("gloo", rank=rank, world_size=world)
+    return tdist
+
+
+def _table_worker(rank, world, port, out):
+    import torch
+
+    import oracle
+    from paper_2508_21287_b200.dist import gather_table, reduce_count, shard_table
+    tdist = _init(rank, world, port)
     try:
-        n, e = g.ibm_heavy_hex(3)
-        k, pe = g.path(7)
-        # oracle roots are its first pattern vertex (order[0]); work prefix = arcs per vertex
-        deg = np.bincount(np.concatenate([e[:, 0], e[:, 1]]), minlength=n)
-        wp = np.concatenate([[0], np.cumsum(deg)])
-
-        def local(b, ee):
-            r = oracle.match(n, e, k, pe, roots=(b, ee), threads=1)
-            return r.count, r.rows
-
-        cnt, rows = match_sharded(local, wp, k, rank=rank, world=world, table=True)
-        full = oracle.match(n, e, k, pe, threads=1)
-        out.put((rank, cnt == full.count, bool(np.array_equal(rows, full.rows))))
+        ok = True
+        for (n, e), (k, pe) in [(g.ibm_heavy_hex(3), g.path(7)), (g.grid_diag(12), g.ring(4)),
+                                (g.er_gnm(40, 160, 3), g.clique(3))]:
+            full = oracle.match(n, e, k, pe, threads=1)
+            # oracle roots are its first pattern vertex; any cut of [0, n) partitions the result
+            cuts = [0] + [n * r // world for r in range(1, world)] + [n]
+            part = oracle.match(n, e, k, pe, roots=(cuts[rank], cuts[rank + 1]), threads=1)
+            total = reduce_count(part.count)                                     # C3
+            # a rank's table in canonical order, then C4 with the splitters cuts[1..world-1]
+            mine = shard_table(torch.from_numpy(part.rows), cuts, n, rank=rank, world=world,
+                               partition=cpu_partition_by_key, sort=cpu_sort)
+            col0 = mine[:, 0].numpy()
+            ok &= bool(np.all((col0 >= cuts[rank]) & (col0 < cuts[rank + 1])))
+            got = gather_table(mine)
+            ok &= total == full.count and bool(np.array_equal(got, full.rows))
+        out.put((rank, ok))
     finally:
         tdist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_sharded_match_gloo(world):
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
-    assert all(c and t for _, c, t in res), res
-
-
-def test_merge_tables():
-    a = np.array([[3, 1], [0, 2]], np.int32)
-    b = np.array([[1, 5]], np.int32)
-    m = merge_tables([a, b, np.zeros((0, 2), np.int32)], 2)
-    assert m.tolist() == [[0, 2], [1, 5], [3, 1]]
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_table_gloo(world):
+    """Seed shards (roots) -> C3 count + C4 range partition / exchange / sort: the rank-order
+    concatenation equals the unsharded canonical table."""
+    res = _spawn(_table_worker, world)
+    assert all(ok for _, ok in res), res
 
 
 def _rebalance_worker(rank, world, port, out):
     import torch
-    import torch.distributed as tdist
+
     from paper_2508_21287_b200.dist import rebalance_rows
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    tdist = _init(rank, world, port)
     try:
-        g = torch.Generator().manual_seed(100 + rank)
+        gen = torch.Generator().manual_seed(100 + rank)
         n = [37, 5, 0][rank % 3] if world == 3 else [40, 3][rank]
-        rows = torch.randint(0, 1000, (n, 4), generator=g, dtype=torch.int32)
+        rows = torch.randint(0, 1000, (n, 4), generator=gen, dtype=torch.int32)
         rows[:, 0] = rank * 1000 + torch.arange(n, dtype=torch.int32)   # unique row ids
-        work = torch.randint(1, 50, (n,), generator=g, dtype=torch.int64)
-        got = rebalance_rows(rows, work, rank=rank, world=world)
-        # gather everything (pickled) to check conservation and balance
+        work = torch.randint(1, 50, (n,), generator=gen, dtype=torch.int64)
+        got = rebalance_rows(rows, work, int(work.sum()), rank=rank, world=world,
+                             partition=cpu_partition_by_work)
         everything = [None] * world
         tdist.all_gather_object(everything, (rows.tolist(), work.tolist(), got.tolist()))
         idmap, before, after = {}, [], []
@@ -115,14 +147,16 @@ def _rebalance_worker(rank, world, port, out):
 @pytest.mark.parametrize("world", [2, 3])
 def test_rebalance_rows_gloo(world):
     """C1 + C2: rows are conserved and every rank ends with ~1/world of the total work."""
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    res = [q.get(timeout=120) for _ in range(world)]
-    for p in procs:
-        p.join(timeout=60)
-        assert p.exitcode == 0
+    res = _spawn(_rebalance_worker, world)
     assert all(ok1 and ok2 for _, ok1, ok2 in res), res
+
+
+def test_cpu_reference_partitions():
+    """The test-side partition definitions themselves (stable grouping, counts)."""
+    import torch
+    rows = torch.tensor([[5, 0], [1, 1], [9, 2], [3, 3]], dtype=torch.int32)
+    p, c = cpu_partition_by_key(rows, 0, [4], 2)
+    assert c == [2, 2] and p[:, 1].tolist() == [1, 3, 0, 2]
+    w = torch.tensor([1, 1, 1, 1], dtype=torch.int64)
+    p, c = cpu_partition_by_work(rows, w, 0, 4, 2)
+    assert c == [2, 2] and p[:, 1].tolist() == [0, 1, 2, 3]

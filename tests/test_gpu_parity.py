@@ -339,13 +339,15 @@ def test_seed_ranges_partition(dm):
 
 def test_prefix_resume_split(dm):
     """dm_match_prefix + dm_match_resume: a level cut into two row sets and finished separately
-    gives the full result (the multi-GPU frontier exchange contract)."""
+    gives the oracle's result (the multi-GPU frontier exchange contract)."""
     import torch
     cases = [(g.ibm_heavy_hex(6), g.path(11), False), (g.rmat(10, 16, seed=3), g.diamond(), True),
              (g.grid_diag(20), g.ring(5), False), (g.er_gnm(300, 2000, 4), g.clique(4), False)]
     for (n, e), (k, pe), drop in cases:
         G = dm.Graph(n, e, drop_self_loops=drop)
         full = G.match(k, pe, output="both")
+        o = oracle.match(n, e, k, pe, drop_self_loops=drop)
+        assert full.count == o.count and np.array_equal(full.rows, o.rows)
         nsteps = dm.Plan(k, pe, stats=G.stats(count_only=False)).num_steps
         assert nsteps == full.stats["num_steps"]
         assert dm.Plan(k, pe, stats=G.stats()).num_steps == G.match(k, pe).stats["num_steps"]
@@ -359,12 +361,14 @@ def test_prefix_resume_split(dm):
             cut = fr.rows // 3
             a = G.match_resume(k, pe, step, rows[:cut].contiguous(), output="both")
             b = G.match_resume(k, pe, step, rows[cut:].contiguous(), output="both")
-            assert a.count + b.count == full.count
+            assert a.count + b.count == o.count
             cat = np.concatenate([a.rows, b.rows])
             cat = cat[np.lexsort(cat.T[::-1])]
-            assert np.array_equal(cat, full.rows)
+            assert np.array_equal(cat, o.rows)
             c = G.match_resume(k, pe, step, rows, output="both")
-            assert c.count == full.count
+            assert c.count == o.count
+            with pytest.raises(ValueError):   # wrong layout is rejected before the library call
+                G.match_resume(k, pe, step, rows[:, :-1].contiguous(), output="both")
     with pytest.raises(dm.DMError):
         G.match_prefix(k, pe, 0)
 
