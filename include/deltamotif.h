@@ -64,14 +64,26 @@ typedef enum {
 
 enum { DM_MONO = 0, DM_INDUCED = 1 };                      /* isomorphism variant (DESIGN Q1) */
 enum { DM_OUT_COUNT = 1, DM_OUT_TABLE = 2 };               /* output bit flags                */
-enum { DM_MOTIF_M2 = 1, DM_MOTIF_M3 = 2, DM_MOTIF_M3O = 4 }; /* planner motif set (bitmask);
-                                                              M2 = edge, M3 = wedge (2-path),
-                                                              M3-O = triangle        */
+/* Planner motif set (bitmask).  P:180 naming: M_i = path of i vertices, "-O" = cycle.
+ * M2 = edge, M3 = wedge, M3-O = triangle are joined implicitly on the CSR; the larger
+ * motifs are materialized tables Res(M) built by Delta-Motif itself (Alg. 2, P:264-279:
+ * dm_graph_build_motifs, or lazily by the first dm_match that asks for them) and joined by
+ * table steps.  The paper's topology-aware sets: {M2, M4} heavy-hex,
+ * {M2, M4-O, M6-O} square grid; M12-O for heavy-hex hexagons. */
+enum {
+  DM_MOTIF_M2 = 1, DM_MOTIF_M3 = 2, DM_MOTIF_M3O = 4,
+  DM_MOTIF_M4 = 8, DM_MOTIF_M5 = 16, DM_MOTIF_M6 = 32, DM_MOTIF_M7 = 64, DM_MOTIF_M8 = 128,
+  DM_MOTIF_M4O = 256, DM_MOTIF_M6O = 512, DM_MOTIF_M12O = 1024
+};
+#define DM_MOTIF_IMPLICIT (DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O)
+#define DM_MOTIF_TABLES (DM_MOTIF_M4 | DM_MOTIF_M5 | DM_MOTIF_M6 | DM_MOTIF_M7 | DM_MOTIF_M8 | \
+                         DM_MOTIF_M4O | DM_MOTIF_M6O | DM_MOTIF_M12O)
+#define DM_MAX_MOTIF_VERTICES 12
 enum { DM_GRAPH_DROP_SELF_LOOPS = 1 };                     /* dm_graph_create flags           */
 enum { DM_MATCH_PROFILE = 1 };                             /* dm_match_opts.flags: time every
                                                               kernel with CUDA events          */
 
-typedef struct {
+typedef struct dm_match_opts_s {
   int32_t mode;        /* DM_MONO (default) or DM_INDUCED                                     */
   int32_t output;      /* DM_OUT_COUNT and/or DM_OUT_TABLE (default DM_OUT_COUNT)             */
   int32_t motifs;      /* planner motif set, bitmask of DM_MOTIF_*; M2 is always added*/
@@ -143,6 +155,23 @@ DM_API int32_t dm_graph_device(const dm_graph *g);
  * probability sampled on 4,096 arcs at creation (pass them to dm_plan_create_ex to reproduce
  * the plan dm_match builds). */
 DM_API dm_status dm_graph_stats(const dm_graph *g, double *sum_d2, double *closure);
+/*
+ * Motif database (Alg. 2 BuildDatabase): Res(M) for every table motif in `motifs`
+ * (DM_MOTIF_M4 ... DM_MOTIF_M12O), each computed by Delta-Motif itself (a table-mode match of the
+ * motif template over {M2, M3, M3-O}), stored on g's device in canonical order and indexed by the
+ * CSR arc of the first two template positions.  Already built tables are kept; the build is the
+ * paper's data-preparation phase (GPU vs GPU*).  dm_match builds what it needs on first
+ * use; thread-safe.  opt: stream and row_budget (max rows per table, default 2^28); may be NULL.
+ * Errors: DM_ERR_ARG (unknown motif bit), DM_ERR_ROW_BUDGET, DM_ERR_OOM, DM_ERR_CUDA.
+ *   dm_graph_motif_rows: |Res(M)| of a built table, -1 if not built.
+ *   dm_graph_motif_build_ms: host wall time the build took, -1 if not built.
+ *   dm_graph_motif_table: copy Res(M) to HOST rows_out[rows][L] (template position order, rows
+ *       ascending lexicographic) and/or the index toff_out[num_arcs + 1] (either may be NULL).
+ */
+DM_API dm_status dm_graph_build_motifs(dm_graph *g, int32_t motifs, const dm_match_opts *opt);
+DM_API int64_t dm_graph_motif_rows(const dm_graph *g, int32_t motif);
+DM_API double dm_graph_motif_build_ms(const dm_graph *g, int32_t motif);
+DM_API dm_status dm_graph_motif_table(const dm_graph *g, int32_t motif, int32_t *rows_out, int64_t *toff_out);
 /* Device pointers of the CSR (owned by g, valid until dm_graph_destroy). */
 DM_API dm_status dm_graph_device_csr(const dm_graph *g, const int64_t **d_off, const int32_t **d_adj);
 /* Copy the CSR to host buffers off_out[n+1] and adj_out[num_arcs] (either may be NULL). */
@@ -292,10 +321,12 @@ DM_API dm_status dm_plan_create_ex(int32_t k, const int32_t *p_edges, int64_t pm
                                    dm_plan **out);
 DM_API void dm_plan_destroy(dm_plan *p);
 DM_API int32_t dm_plan_num_slices(const dm_plan *p);
-/* Slice i: motif id (DM_MOTIF_*), its pattern vertices (slot order, n_vertices <= 3) and the
- * join constraints = vertices shared with the union of earlier slices. */
+/* Slice i: motif id (DM_MOTIF_*), its pattern vertices (template position order, n_vertices <=
+ * DM_MAX_MOTIF_VERTICES) and the join constraints = vertices shared with the union of earlier
+ * slices (decomposition order). */
 DM_API dm_status dm_plan_slice(const dm_plan *p, int32_t i, int32_t *motif, int32_t *n_vertices,
-                        int32_t vertices[3], int32_t *n_constraints, int32_t constraints[3]);
+                               int32_t vertices[DM_MAX_MOTIF_VERTICES], int32_t *n_constraints,
+                               int32_t constraints[DM_MAX_MOTIF_VERTICES]);
 DM_API int32_t dm_plan_num_steps(const dm_plan *p);          /* executed kernel steps             */
 DM_API int32_t dm_plan_first_vertex(const dm_plan *p);       /* pattern vertex sharded by seed    */
 /* Human-readable JSON description of slices and steps (for tests / debugging).  Writes at

@@ -28,6 +28,10 @@ ERRORS = {-1: "DM_ERR_ARG", -2: "DM_ERR_VERTEX_RANGE", -3: "DM_ERR_SELF_LOOP",
 DM_MONO, DM_INDUCED = 0, 1
 DM_OUT_COUNT, DM_OUT_TABLE = 1, 2
 DM_MOTIF_M2, DM_MOTIF_M3, DM_MOTIF_M3O = 1, 2, 4
+MOTIF_BITS = {"M2": 1, "M3": 2, "M3-O": 4, "M4": 8, "M5": 16, "M6": 32, "M7": 64, "M8": 128,
+              "M4-O": 256, "M6-O": 512, "M12-O": 1024}
+MOTIF_NAMES = {v: k for k, v in MOTIF_BITS.items()}
+DM_MAX_MOTIF_VERTICES = 12
 DM_GRAPH_DROP_SELF_LOOPS = 1
 DM_MATCH_PROFILE = 1
 DM_MAX_PATTERN = 128
@@ -35,10 +39,13 @@ DM_MAX_STEPS = 128
 ABI_VERSION = 3
 
 MOTIF_SETS = {
-    "all": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O,
+    "all": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O,   # the implicit (CSR-joined) motifs
     "M2": DM_MOTIF_M2,
     "M3": DM_MOTIF_M2 | DM_MOTIF_M3,
     "M3O": DM_MOTIF_M2 | DM_MOTIF_M3O,
+    # the paper's topology-aware sets: heavy-hex {M2, M4}, square grid {M2, M4-O, M6-O}
+    "heavy-hex": DM_MOTIF_M2 | 8,
+    "grid": DM_MOTIF_M2 | 256 | 512,
 }
 
 
@@ -86,7 +93,8 @@ EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_
            "dm_frontier_free", "dm_match_resume", "dm_frontier_work_total", "dm_plan_create_for",
            "dm_plan_width", "dm_plan_stride", "dm_plan_column_vertex", "dm_plan_seed_work",
            "dm_plan_seed_cuts", "dm_plan_seed", "dm_plan_step", "dm_plan_finish_table", "dm_plan_run",
-           "dm_rows_partition_by_work", "dm_rows_partition_by_key", "dm_table_sort"]
+           "dm_rows_partition_by_work", "dm_rows_partition_by_key", "dm_table_sort",
+           "dm_graph_build_motifs", "dm_graph_motif_rows", "dm_graph_motif_build_ms", "dm_graph_motif_table"]
 
 
 def lib():
@@ -158,6 +166,10 @@ def lib():
         "dm_rows_partition_by_key": (c.c_int, [P, c.c_int64, c.c_int32, c.c_int32, P, c.c_int32, P, P,
                                                P]),
         "dm_table_sort": (c.c_int, [P, c.c_int64, c.c_int32, c.c_int32, P]),
+        "dm_graph_build_motifs": (c.c_int, [P, c.c_int32, c.POINTER(_Opts)]),
+        "dm_graph_motif_rows": (c.c_int64, [P, c.c_int32]),
+        "dm_graph_motif_build_ms": (c.c_double, [P, c.c_int32]),
+        "dm_graph_motif_table": (c.c_int, [P, c.c_int32, P, P]),
     }
     for name, (rt, args) in sig.items():
         f = getattr(L, name)
@@ -180,8 +192,14 @@ def _edges_arr(edges) -> np.ndarray:
 
 
 def _motifs(m) -> int:
+    """Motif set: a MOTIF_SETS name, a comma list of motif names ("M2,M3,M5"), or a bitmask."""
     if isinstance(m, str):
-        return MOTIF_SETS[m]
+        if m in MOTIF_SETS:
+            return MOTIF_SETS[m]
+        bits = 0
+        for name in m.split(","):
+            bits |= MOTIF_BITS[name.strip()]
+        return bits
     return int(m)
 
 
@@ -364,10 +382,11 @@ class Plan:
     def slices(self):
         L = lib()
         out = []
-        names = {1: "M2", 2: "M3", 4: "M3-O"}
+        names = MOTIF_NAMES
         for i in range(L.dm_plan_num_slices(self._h)):
             m, nv, nc = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
-            vs, cs = (ctypes.c_int32 * 3)(), (ctypes.c_int32 * 3)()
+            vs = (ctypes.c_int32 * DM_MAX_MOTIF_VERTICES)()
+            cs = (ctypes.c_int32 * DM_MAX_MOTIF_VERTICES)()
             _check(L.dm_plan_slice(self._h, i, ctypes.byref(m), ctypes.byref(nv), vs, ctypes.byref(nc), cs))
             out.append({"motif": names[m.value], "vertices": list(vs)[:nv.value],
                         "constraints": list(cs)[:nc.value]})
@@ -483,6 +502,31 @@ class Graph:
     @property
     def device(self) -> int:
         return lib().dm_graph_device(self._h)
+
+    def build_motifs(self, motifs, *, stream=None, row_budget: int = 0) -> dict:
+        """dm_graph_build_motifs: the motif database (Alg. 2) for the table motifs of `motifs`;
+        returns {name: (rows, build_ms)}."""
+        bits = _motifs(motifs)
+        o = self._opts("mono", "count", bits, None, stream, False, 0, row_budget)
+        _check(lib().dm_graph_build_motifs(self._h, bits, ctypes.byref(o)))
+        return {MOTIF_NAMES[b]: (self.motif_rows(b), lib().dm_graph_motif_build_ms(self._h, b))
+                for b in MOTIF_NAMES if b >= 8 and bits & b}
+
+    def motif_rows(self, motif) -> int:
+        b = MOTIF_BITS[motif] if isinstance(motif, str) else int(motif)
+        return int(lib().dm_graph_motif_rows(self._h, b))
+
+    def motif_table(self, motif):
+        """(rows [R][L] int32 canonical, toff [num_arcs + 1] int64) of a built table (host copies)."""
+        b = MOTIF_BITS[motif] if isinstance(motif, str) else int(motif)
+        R = self.motif_rows(b)
+        if R < 0:
+            raise DMError(-1, "motif table not built")
+        Lv = {8: 4, 16: 5, 32: 6, 64: 7, 128: 8, 256: 4, 512: 6, 1024: 12}[b]
+        rows = np.zeros((R, Lv), dtype=np.int32)
+        toff = np.zeros(self.num_arcs + 1, dtype=np.int64)
+        _check(lib().dm_graph_motif_table(self._h, b, rows.ctypes.data if R else None, toff.ctypes.data))
+        return rows, toff
 
     def plan(self, k: int, p_edges, **kw) -> Plan:
         """dm_plan_create_for: the join program dm_match runs for this pattern."""

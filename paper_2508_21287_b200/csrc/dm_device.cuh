@@ -5,9 +5,32 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 #include <string>
 
 #include "dm_internal.h"
+
+namespace dm {
+// A materialized motif table Res(M) (Alg. 2) on the device: every embedding of the
+// template (rows = labelled embeddings, columns = template positions), rows in ascending
+// lexicographic order, 16-byte row stride (padding -1); the arc index toff[arc] = first row whose
+// (position 0, position 1) pair is >= that CSR arc, so the rows keyed by a vertex a are
+// [toff[off[a]], toff[off[a+1]]) and those keyed by an arc (a,b) [toff[arc], toff[arc+1]).
+struct MotifTable {
+  int motif = 0;            // DM_MOTIF_* bit
+  int L = 0;                // template vertices
+  int stride = 0;           // int32 words per row (round_up(L, 4))
+  int64_t rows = 0;
+  int32_t *d_rows = nullptr;
+  int64_t *d_toff = nullptr;  // [arcs + 1]
+  double build_ms = 0.0;
+};
+struct TabStore {
+  std::mutex mu;
+  MotifTable t[32];  // by motif bit index
+};
+int motif_bit(int id);  // bit index of a DM_MOTIF_* id
+}  // namespace dm
 
 struct dm_graph {
   int device = 0;
@@ -20,6 +43,7 @@ struct dm_graph {
   double sum_d2 = 0.0;       // sum of squared degrees (size-biased degree = sum_d2 / arcs)
   double closure = 0.0;      // sampled P[c in N(a) | a-b-c wedge] (triangle closure)
   uint64_t gen = 0;          // process-unique creation id (keys host-side caches)
+  dm::TabStore *tabs = nullptr;  // motif database (Alg. 2), built on demand
 };
 
 namespace dm {
@@ -134,5 +158,27 @@ cudaError_t launch_agg_to_excl(const unsigned long long *agg, int64_t tiles, uin
                                cudaStream_t s);
 
 DevStep make_dev_step(const Step &st);
+
+// ---- table steps (tabstep.cu): one slice's fresh vertices joined with Res(M) (Step::tab_motif)
+struct DevTabStep {
+  int32_t in_w, n_new;
+  int32_t key0, key1, skip;  // row columns bound to template positions 0 / 1; known-duplicate column
+  int32_t L, tstride;        // template vertices, table row stride (words)
+  int32_t n_eq, n_pr;
+  uint32_t newmask;          // bit p: template position p is a new vertex
+  uint32_t eqmask;           // bit p: template position p must equal row[eq_colp[p]]
+  int8_t newpos[kMaxMotifV];
+  int8_t eq_pos[kMaxMotifV];
+  uint8_t eq_col[kMaxMotifV];
+  uint8_t eq_colp[kMaxMotifV];
+  uint8_t colpos[kMaxMotifV];  // new template position p -> new column index (w + colpos[p])
+  uint8_t pr_j[kMaxTabProbes], pr_c[kMaxTabProbes], pr_neg[kMaxTabProbes];
+};
+DevTabStep make_dev_tab_step(const Step &st, const MotifTable &t);
+cudaError_t launch_table(int mode, const DevTabStep &st, const StepIO &io, const dm_graph &g,
+                         const MotifTable &t, int64_t num_tiles, cudaStream_t s);
+// table construction helpers: repack a canonical [rows][L] table to the 16-byte stride and build
+// the arc index (tabstep.cu)
+dm_status finish_motif_table(const dm_graph &g, int32_t *packed, int64_t rows, MotifTable &t, cudaStream_t s);
 
 }  // namespace dm

@@ -15,14 +15,30 @@ dm_status fail(dm_status code, const std::string &msg);  // sets the thread-loca
 void clear_error();
 
 // ---------------------------------------------------------------------------- planner
+// Motif templates (P:180 naming: M_i = path of i vertices, "-O" = cycle).  M2, M3 and M3-O are
+// joined implicitly on the CSR (Res(M3) = Res(M2) ⋈ Res(M2)); the larger ones are
+// materialized tables Res(M) built by Delta-Motif itself (Alg. 2) and joined by
+// table steps.
+constexpr int kMaxMotifV = DM_MAX_MOTIF_VERTICES;
+struct MotifDef {
+  int id;      // DM_MOTIF_* bit
+  int nv;      // template vertices 0..nv-1
+  bool cycle;  // edges i-(i+1) (+ (nv-1)-0 for a cycle)
+  const char *name;
+};
+const MotifDef *motif_def(int id);           // nullptr for an unknown bit
+const std::vector<const MotifDef *> &motif_defs();  // every motif, decomposition order
+inline bool motif_is_table(int id) { return id >= DM_MOTIF_M4; }
+
 // One motif slice S_i of the decomposition: motif template, the pattern
-// vertices it is matched onto (slot order) and the join constraints (shared vertices).
+// vertices it is matched onto (template position order) and the join constraints (shared
+// vertices).
 struct Slice {
-  int motif = DM_MOTIF_M2;  // DM_MOTIF_M2 / DM_MOTIF_M3 / DM_MOTIF_M3O
+  int motif = DM_MOTIF_M2;
   int nv = 0;
-  int v[3] = {-1, -1, -1};
+  int v[kMaxMotifV];
   int nc = 0;
-  int c[3] = {-1, -1, -1};
+  int c[kMaxMotifV];
 };
 
 // A vertex placed by an executed step: the join key columns it must be adjacent to (the
@@ -37,18 +53,40 @@ struct StepVertex {
   int non[DM_MAX_PATTERN];
 };
 
-// One executed join step: 1 or 2 new vertices (up to kMaxNew for a count-only last step on a
-// max-degree-4 graph, where the tail kernel enumerates them without materializing the levels).
+// One executed join step.  CSR step (tab_motif == 0): 1 or 2 new vertices (up to kMaxNew for a
+// count-only last step on a max-degree-4 graph, where the tail kernel enumerates them without
+// materializing the levels).  Table step (tab_motif != 0): the fresh vertices of one slice S
+// joined with Res(M_S) (Alg. 1 l.6 InnerJoin): the row's image of the pattern vertex on
+// template position 0 (and 1, key1 >= 0) selects the index range of the table; further bound
+// template positions are equality filters (the remaining join constraints);
+// pattern edges the motif does not cover are closing-edge probes (and non-edges in induced
+// mode); the all-distinct filter covers the new vertices.
 constexpr int kMaxNew = 4;
+constexpr int kMaxTabProbes = 256;
+struct TabProbe {
+  int j;    // new vertex (0-based within the step)
+  int col;  // row column it is probed against (may be a new column in_w + j' with j' < j)
+  int neg;  // 1: must NOT be adjacent (induced non-edge)
+};
 struct Step {
   int slice = -1;
   int in_w = 0;
   int n_new = 0;
   StepVertex nv[kMaxNew];
+  // table step
+  int tab_motif = 0;
+  int key0 = -1, key1 = -1;      // row columns bound to template positions 0 and 1 (key1 < 0: one key)
+  int skip = -1;                 // one-key step: a column whose image, as template position 1, is a
+                                 // known duplicate (a pattern neighbour of the key): skipped range
+  int newpos[kMaxMotifV];        // template position of new column in_w + j
+  int n_eq = 0;
+  int eq_pos[kMaxMotifV], eq_col[kMaxMotifV];  // template position eq_pos[i] must equal row[eq_col[i]]
+  std::vector<TabProbe> probes;
 };
 
 // Data-graph statistics for the join-order cost model (defaults: a sparse lattice).
 struct PlanStats {
+  double tab_rows[32] = {};  // |Res(M)| of built motif tables, by DM_MOTIF_* bit index (0 = estimate)
   double n = 10000.0;
   double avg_degree = 3.0;   // arcs / n: expansion from the implicit vertex table
   double fwd_degree = 3.0;   // sum d^2 / arcs: degree of a vertex reached along an edge

@@ -744,6 +744,11 @@ DevStep make_dev_step(const Step &st) {
   DevStep d{};
   d.in_w = st.in_w;
   d.n_new = st.n_new;
+  if (st.tab_motif) {  // table step: widths + the key (per-row work estimate of k_row_work)
+    d.n_nbr[0] = 1;
+    d.nbr[0][0] = (uint8_t)st.key0;
+    return d;
+  }
   for (int j = 0; j < st.n_new; ++j) {
     d.n_nbr[j] = st.nv[j].n_nbr;
     d.n_non[j] = st.nv[j].n_non;

@@ -145,6 +145,11 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   static std::atomic<uint64_t> next_gen{1};
   if (g) g->gen = next_gen.fetch_add(1);
   if (!g) return fail(DM_ERR_OOM, "host allocation failed");
+  g->tabs = new (std::nothrow) TabStore;
+  if (!g->tabs) {
+    delete g;
+    return fail(DM_ERR_OOM, "host allocation failed");
+  }
   g->device = device;
   g->n = n;
   const int64_t nk = 2 * m;
@@ -167,6 +172,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
     cudaFree(g->d_off);
     cudaFree(g->d_adj);
     cudaFree(g->d_ell);
+    delete g->tabs;
     delete g;
     return st;
   };
@@ -276,6 +282,13 @@ dm_status dm_graph_create(int32_t n, const int32_t *edges, int64_t m, int32_t fl
 void dm_graph_destroy(dm_graph *g) {
   if (!g) return;
   dm::DeviceGuard dg(g->device);
+  if (g->tabs) {
+    for (auto &t : g->tabs->t) {
+      cudaFree(t.d_rows);
+      cudaFree(t.d_toff);
+    }
+    delete g->tabs;
+  }
   cudaFree(g->d_off);
   cudaFree(g->d_adj);
   cudaFree(g->d_ell);

@@ -150,6 +150,8 @@ struct Ctx {
   uint64_t live = 0;        // bytes of frontier buffers currently held by the recursion
   uint64_t row_budget = 0;
   std::vector<DevStep> dsteps;
+  std::vector<DevTabStep> tsteps;       // table steps (Step::tab_motif != 0), by step index
+  std::vector<MotifTable> tabs;         //   ... and the motif table each one joins with
   unsigned long long *d_acc = nullptr;  // [slots] count-mode total, then per step i:
                                         //   [C_i slots][Q_i slots] (kAccSlots each)
   int32_t *d_res = nullptr;             // table mode: rows in column (match) order
@@ -169,7 +171,30 @@ struct Ctx {
 // config 5, a 16-bit input level saved 0.1 ms in the producer and cost 1.2 ms in the tail).
 int level_elem(const Ctx &c, int lvl) {
   if (c.elem == 4) return 4;
-  return (lvl == (int)c.plan->steps.size() - 1 && !c.table) ? 4 : 2;
+  const int ns = (int)c.plan->steps.size();
+  if (lvl == ns - 1 && !c.table && !c.plan->steps[(size_t)lvl].tab_motif) return 4;
+  return 2;
+}
+
+// ---- per-step kernel dispatch: table steps (tabstep.cu) or CSR steps (extend.cu / tail.cu /
+// pairs.cu)
+bool is_tab(const Ctx &c, int si) { return c.plan->steps[(size_t)si].tab_motif != 0; }
+// single-pass launches that reserve output space atomically (no look-back status words)
+bool atomic_step(const Ctx &c, int si) { return is_tab(c, si) || row_serial_step(c.dsteps[(size_t)si], *c.g); }
+cudaError_t launch_count_step(const Ctx &c, int si, const StepIO &io, int64_t tiles) {
+  if (is_tab(c, si)) return launch_table(kModeCount, c.tsteps[(size_t)si], io, *c.g, c.tabs[(size_t)si], tiles, c.s);
+  const DevStep &D = c.dsteps[(size_t)si];
+  const int pm = pair_mode_of(D);
+  if (pm >= 0 && !row_serial_step(D, *c.g)) return launch_pairs(D, io, *c.g, pm, c.s);
+  return launch_step_count(D, io, *c.g, tiles, c.s);
+}
+cudaError_t launch_single_step(const Ctx &c, int si, const StepIO &io, int64_t tiles) {
+  if (is_tab(c, si)) return launch_table(kModeSingle, c.tsteps[(size_t)si], io, *c.g, c.tabs[(size_t)si], tiles, c.s);
+  return launch_step_single(c.dsteps[(size_t)si], io, *c.g, tiles, c.s);
+}
+cudaError_t launch_write_step(const Ctx &c, int si, const StepIO &io, int64_t tiles) {
+  if (is_tab(c, si)) return launch_table(kModeWrite, c.tsteps[(size_t)si], io, *c.g, c.tabs[(size_t)si], tiles, c.s);
+  return launch_step_write(c.dsteps[(size_t)si], io, *c.g, tiles, c.s);
 }
 
 dm_status cuda_fail(cudaError_t e, const char *what) {
@@ -231,7 +256,7 @@ dm_status write_tiles(Ctx &c, int si, const StepIO &base_io, const uint64_t *d_e
   io.total = nullptr;
   Prof::Ev e;
   c.prof.begin(si, 1, e);
-  CK(launch_step_write(c.dsteps[(size_t)si], io, *c.g, b1 - b0, c.s), "write kernel");
+  CK(launch_write_step(c, si, io, b1 - b0), "write kernel");
   c.prof.end(e);
   c.st.num_launches++;
   return DM_OK;
@@ -280,11 +305,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
     io.total = c.d_acc;
     Prof::Ev e;
     c.prof.begin(si, 0, e);
-    const int pm = pair_mode_of(D);
-    if (pm >= 0 && !row_serial_step(D, *c.g))
-      CK(launch_pairs(D, io, *c.g, pm, c.s), "pair kernel");
-    else
-      CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
+    CK(launch_count_step(c, si, io, tiles), "count kernel");
     c.prof.end(e);
     c.st.num_launches++;
     return DM_OK;
@@ -326,7 +347,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   CK(status.alloc((size_t)tiles, c.s), "status");
   CK(agg.alloc((size_t)tiles + 1, c.s), "agg");
   CK(ctrl.alloc(3, c.s), "ctrl");
-  if (!row_serial_step(D, *c.g))  // look-back status words (candidate-partitioned kernel)
+  if (!atomic_step(c, si))  // look-back status words (candidate-partitioned kernel)
     CK(cudaMemsetAsync(status.p, 0, sizeof(unsigned long long) * (size_t)tiles, c.s), "memset");
   CK(cudaMemsetAsync(agg.p + tiles, 0, sizeof(unsigned long long), c.s), "memset");
   CK(cudaMemsetAsync(ctrl.p, 0, 3 * sizeof(unsigned long long), c.s), "memset");
@@ -339,7 +360,7 @@ dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t s
   {
     Prof::Ev e;
     c.prof.begin(si, 1, e);
-    CK(launch_step_single(D, io, *c.g, tiles, c.s), "single-pass kernel");
+    CK(launch_single_step(c, si, io, tiles), "single-pass kernel");
     c.prof.end(e);
     c.st.num_launches++;
   }
@@ -446,7 +467,7 @@ bool async_eligible(const Ctx &c) {
   const int nsteps = (int)c.plan->steps.size();
   if (c.table || c.stop_at >= 0 || nsteps < 2) return false;
   for (int si = 0; si + 1 < nsteps; ++si)
-    if (!row_serial_step(c.dsteps[(size_t)si], *c.g)) return false;  // atomic-reservation kernels
+    if (!atomic_step(c, si)) return false;  // atomic-reservation kernels
   return true;
 }
 
@@ -494,11 +515,7 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
       io.total = c.d_acc;
       Prof::Ev e;
       c.prof.begin(si, 0, e);
-      const int pm = pair_mode_of(D);
-      if (pm >= 0 && !row_serial_step(D, *c.g))
-        CK(launch_pairs(D, io, *c.g, pm, c.s), "pair kernel");
-      else
-        CK(launch_step_count(D, io, *c.g, tiles, c.s), "count kernel");
+      CK(launch_count_step(c, si, io, tiles), "count kernel");
       c.prof.end(e);
       c.st.num_launches++;
     } else {
@@ -513,7 +530,7 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
       io.agg = agg;
       Prof::Ev e;
       c.prof.begin(si, 1, e);
-      cudaError_t err = launch_step_single(D, io, *c.g, tiles, c.s);
+      cudaError_t err = launch_single_step(c, si, io, tiles);
       c.prof.end(e);
       c.st.num_launches++;
       cudaFreeAsync(agg, c.s);
@@ -552,7 +569,7 @@ dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows,
 // Permute columns to pattern order and sort rows lexicographically (LSD radix sort over the
 // columns, last column first).  Writes the device table `d_out` [n][k] (or,
 // with d_out == nullptr, the host rows).
-dm_status canonicalize(Ctx &c, int32_t *host_out, int32_t *d_out = nullptr) {
+dm_status canonicalize(Ctx &c, int32_t *host_out, int32_t *d_out = nullptr, int32_t **d_owned = nullptr) {
   const int k = c.plan->k;
   const int64_t n = (int64_t)c.res_rows;
   if (n == 0) return DM_OK;
@@ -563,6 +580,10 @@ dm_status canonicalize(Ctx &c, int32_t *host_out, int32_t *d_out = nullptr) {
   if (!dst) {
     CK(outb.alloc((size_t)n * k, c.s), "canonical table");
     dst = outb.p;
+    if (d_owned) {  // the caller takes the device table
+      *d_owned = outb.p;
+      outb.p = nullptr;
+    }
   }
   dm_status st = lex_sort_rows(c.d_res, n, row_stride(k), c.plan->pvert_col.data(), k, id_bits(c.g->n), dst, c.s);
   if (st != DM_OK) return st;
@@ -586,6 +607,8 @@ dm_status cached_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t mot
     std::snprintf(buf, sizeof(buf), "%d|%d|%d|%.9g|%.9g|%.9g|%.9g|%d|%d|", k, motifs, mode, st.n,
                   st.avg_degree, st.fwd_degree, st.closure, (int)st.count_only, st.max_degree);
     key = buf;
+    for (int b = 0; b < 32; ++b)
+      if (st.tab_rows[b] > 0) key += std::to_string(b) + ":" + std::to_string((long long)st.tab_rows[b]) + "|";
     key.append(reinterpret_cast<const char *>(p_edges), (size_t)pm * 2 * sizeof(int32_t));
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
@@ -651,9 +674,60 @@ __global__ void k_row_work(const int32_t *__restrict__ rows, int64_t n, int stri
       best = d < best ? d : best;
     }
     unsigned long long wk = 1;
-    for (int j = 0; j < st.n_new; ++j) wk *= (best + 1);
+    for (int j = 0; j < st.n_new && j < kMaxNew; ++j) wk *= (best + 1);
     work[i] = wk;
   }
+}
+
+
+// ---------------------------------------------------------------------------------------
+// Motif database (Alg. 2): Res(M) of each requested table motif is computed by
+// Delta-Motif itself -- a table-mode match of the motif template with the implicit motifs
+// {M2, M3, M3-O} (e.g. Res(M4) = Res(M3) ⋈ Res(M2)) -- kept on the device in canonical
+// (lexicographic) order, and indexed by the CSR arc of its first two template positions.
+dm_status build_motif_table(const dm_graph *g, int id, cudaStream_t s, uint64_t row_budget, MotifTable &t);
+
+// Builds the missing tables of `motifs` (thread-safe; built tables are immutable).
+dm_status ensure_tables(const dm_graph *g, int motifs, cudaStream_t s, uint64_t row_budget) {
+  if (!(motifs & DM_MOTIF_TABLES)) return DM_OK;
+  std::lock_guard<std::mutex> lk(g->tabs->mu);
+  for (const MotifDef *M : motif_defs()) {
+    if (!(motifs & M->id) || !motif_is_table(M->id)) continue;
+    MotifTable &t = g->tabs->t[motif_bit(M->id)];
+    if (t.d_toff) continue;
+    MotifTable nt;
+    dm_status st = build_motif_table(g, M->id, s, row_budget, nt);
+    if (st != DM_OK) return st;
+    t = nt;
+  }
+  return DM_OK;
+}
+
+dm_status ensure_tables_on(const dm_graph *g, const dm_match_opts &o) {
+  DeviceGuard dg(g->device);
+  if (!dg.ok) return fail(DM_ERR_CUDA, "cudaSetDevice failed");
+  return ensure_tables(g, o.motifs, (cudaStream_t)o.cuda_stream, o.row_budget ? o.row_budget : (1ull << 28));
+}
+
+MotifTable table_of(const dm_graph *g, int id) {
+  std::lock_guard<std::mutex> lk(g->tabs->mu);
+  return g->tabs->t[motif_bit(id)];
+}
+
+PlanStats graph_plan_stats(const dm_graph *g, bool count_only, int motifs) {
+  PlanStats ps;
+  ps.n = (double)std::max<int32_t>(g->n, 2);
+  ps.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
+  ps.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
+  ps.closure = g->closure;
+  ps.count_only = count_only;
+  ps.max_degree = g->max_deg;
+  if (motifs & DM_MOTIF_TABLES) {
+    std::lock_guard<std::mutex> lk(g->tabs->mu);
+    for (int b = 0; b < 32; ++b)
+      if ((motifs >> b) & 1) ps.tab_rows[b] = g->tabs->t[b].d_toff ? std::max(0.5, (double)g->tabs->t[b].rows) : 0.0;
+  }
+  return ps;
 }
 
 struct FrontierOut {
@@ -673,6 +747,7 @@ struct RunSpec {
   const int32_t *from_rows = nullptr;
   int64_t from_n = 0;
   int32_t *d_canon = nullptr;     // table mode: canonical table to this device buffer [count][k]
+  int32_t **d_canon_owned = nullptr;  // ... or into a new device buffer handed to the caller
   bool no_host_table = false;     //   ... and not to the host
 };
 
@@ -708,13 +783,9 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   const Plan *pp = rs.plan;
   dm_status stt = DM_OK;
   if (!pp) {
-    PlanStats pstats;
-    pstats.n = (double)std::max<int32_t>(g->n, 2);
-    pstats.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
-    pstats.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
-    pstats.closure = g->closure;
-    pstats.count_only = !(opt.output & DM_OUT_TABLE);
-    pstats.max_degree = g->max_deg;
+    stt = ensure_tables_on(g, opt);  // the motif database of the requested set (Alg. 2), built on first use
+    if (stt != DM_OK) return stt;
+    const PlanStats pstats = graph_plan_stats(g, !(opt.output & DM_OUT_TABLE), opt.motifs);
     stt = cached_plan(k, p_edges, pm, opt.motifs, opt.mode, pstats, plan_local);
     if (stt != DM_OK) return stt;
     pp = &plan_local;
@@ -750,7 +821,16 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   c.row_budget = opt.row_budget ? opt.row_budget : (1ull << 27);
   std::memset(&c.st, 0, sizeof(c.st));
   c.st.num_steps = (int32_t)plan.steps.size();
-  for (auto &s : plan.steps) c.dsteps.push_back(make_dev_step(s));
+  for (auto &s : plan.steps) {
+    c.dsteps.push_back(make_dev_step(s));
+    MotifTable t;
+    if (s.tab_motif) {
+      t = table_of(g, s.tab_motif);
+      if (!t.d_toff) return fail(DM_ERR_ARG, "plan joins a motif table this graph has not built (dm_graph_build_motifs)");
+    }
+    c.tabs.push_back(t);
+    c.tsteps.push_back(s.tab_motif ? make_dev_tab_step(s, t) : DevTabStep{});
+  }
   c.ratio.assign(plan.steps.size(), 0.0);
   for (size_t i = 0; i < plan.steps.size(); ++i) {
     c.st.width_in[i] = plan.steps[i].in_w;
@@ -907,7 +987,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
         res->rows = (int32_t *)std::malloc(sizeof(int32_t) * std::max<uint64_t>(count * k, 1));
         if (!res->rows) return fail(DM_ERR_OOM, "host allocation failed");
       }
-      stt = canonicalize(c, rs.no_host_table ? nullptr : res->rows, rs.d_canon);
+      stt = canonicalize(c, rs.no_host_table ? nullptr : res->rows, rs.d_canon, rs.d_canon_owned);
       if (stt != DM_OK) return stt;
     }
   }
@@ -945,6 +1025,43 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
   rg.keep = true;
   *out = res;
   return DM_OK;
+}
+
+dm_status build_motif_table(const dm_graph *g, int id, cudaStream_t s, uint64_t row_budget, MotifTable &t) {
+  const MotifDef *M = motif_def(id);
+  if (!M || !motif_is_table(id)) return fail(DM_ERR_ARG, "not a table motif");
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<int32_t> pe;
+  for (int a = 0; a + 1 < M->nv; ++a) {
+    pe.push_back(a);
+    pe.push_back(a + 1);
+  }
+  if (M->cycle) {
+    pe.push_back(M->nv - 1);
+    pe.push_back(0);
+  }
+  dm_match_opts o;
+  dm_match_opts_init(&o);
+  o.output = DM_OUT_TABLE;
+  o.motifs = DM_MOTIF_IMPLICIT;  // Res(M) from the smaller motifs (Alg. 2 recursion)
+  o.row_budget = std::min<uint64_t>(row_budget, (uint64_t)INT32_MAX);
+  o.cuda_stream = (void *)s;
+  RunSpec rs;
+  rs.no_host_table = true;
+  int32_t *packed = nullptr;
+  rs.d_canon_owned = &packed;
+  dm_result *r = nullptr;
+  dm_status st = match_impl(g, M->nv, pe.data(), (int64_t)pe.size() / 2, &o, &r, rs);
+  if (st != DM_OK) return st;
+  t.motif = id;
+  t.L = M->nv;
+  const int64_t rows = (int64_t)r->count;
+  dm_result_free(r);
+  st = finish_motif_table(*g, packed, rows, t, s);
+  if (packed) cudaFreeAsync(packed, s);
+  cudaStreamSynchronize(s);
+  t.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return st;
 }
 
 dm_status make_frontier(const dm_graph *g, const dm_match_opts *opt, const FrontierOut &fo, dm_frontier **out) {
@@ -1013,14 +1130,10 @@ dm_status dm_match_prefix(const dm_graph *g, int32_t k, const int32_t *p_edges, 
   if (opt) o = *opt;
   dm::Plan probe;
   {
-    dm::PlanStats ps;
-    ps.n = (double)std::max<int32_t>(g->n, 2);
-    ps.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
-    ps.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
-    ps.closure = g->closure;
-    ps.count_only = !(o.output & DM_OUT_TABLE);
-    ps.max_degree = g->max_deg;
-    dm_status st = dm::cached_plan(k, p_edges, pm, o.motifs, o.mode, ps, probe);
+    dm_status st = dm::ensure_tables_on(g, o);
+    if (st != DM_OK) return st;
+    const dm::PlanStats ps = dm::graph_plan_stats(g, !(o.output & DM_OUT_TABLE), o.motifs);
+    st = dm::cached_plan(k, p_edges, pm, o.motifs, o.mode, ps, probe);
     if (st != DM_OK) return st;
   }
   if (upto_step < 1 || upto_step >= (int32_t)probe.steps.size())
@@ -1068,16 +1181,12 @@ dm_status dm_plan_create_for(const dm_graph *g, int32_t k, const int32_t *p_edge
   dm_match_opts o;
   dm_match_opts_init(&o);
   if (opt) o = *opt;
-  dm::PlanStats ps;
-  ps.n = (double)std::max<int32_t>(g->n, 2);
-  ps.avg_degree = g->n ? (double)g->arcs / (double)g->n : 1.0;
-  ps.fwd_degree = g->arcs ? g->sum_d2 / (double)g->arcs : 1.0;
-  ps.closure = g->closure;
-  ps.count_only = !(o.output & DM_OUT_TABLE);
-  ps.max_degree = g->max_deg;
+  dm_status st = dm::ensure_tables_on(g, o);
+  if (st != DM_OK) return st;
+  const dm::PlanStats ps = dm::graph_plan_stats(g, !(o.output & DM_OUT_TABLE), o.motifs);
   dm_plan *p = new (std::nothrow) dm_plan;
   if (!p) return dm::fail(DM_ERR_OOM, "host allocation failed");
-  dm_status st = dm::cached_plan(k, p_edges, pm, o.motifs, o.mode, ps, p->p);
+  st = dm::cached_plan(k, p_edges, pm, o.motifs, o.mode, ps, p->p);
   if (st != DM_OK) {
     delete p;
     return st;
@@ -1178,6 +1287,45 @@ dm_status dm_plan_finish_table(const dm_graph *g, const dm_plan *p, const dm_mat
   if (st != DM_OK) return st;
   cudaError_t e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) return dm::fail(DM_ERR_CUDA, std::string("sync: ") + cudaGetErrorString(e));
+  return DM_OK;
+}
+
+dm_status dm_graph_build_motifs(dm_graph *g, int32_t motifs, const dm_match_opts *opt) {
+  dm::clear_error();
+  if (!g) return dm::fail(DM_ERR_ARG, "graph is NULL");
+  if (motifs & ~(DM_MOTIF_IMPLICIT | DM_MOTIF_TABLES)) return dm::fail(DM_ERR_ARG, "unknown motif bit");
+  dm_match_opts o;
+  dm_match_opts_init(&o);
+  if (opt) o = *opt;
+  o.motifs = motifs;
+  return dm::ensure_tables_on(g, o);
+}
+
+int64_t dm_graph_motif_rows(const dm_graph *g, int32_t motif) {
+  if (!g || !dm::motif_def(motif) || !dm::motif_is_table(motif)) return -1;
+  const dm::MotifTable t = dm::table_of(g, motif);
+  return t.d_toff ? t.rows : -1;
+}
+
+double dm_graph_motif_build_ms(const dm_graph *g, int32_t motif) {
+  if (!g || !dm::motif_def(motif) || !dm::motif_is_table(motif)) return -1.0;
+  const dm::MotifTable t = dm::table_of(g, motif);
+  return t.d_toff ? t.build_ms : -1.0;
+}
+
+dm_status dm_graph_motif_table(const dm_graph *g, int32_t motif, int32_t *rows_out, int64_t *toff_out) {
+  dm::clear_error();
+  if (!g || !dm::motif_def(motif) || !dm::motif_is_table(motif)) return dm::fail(DM_ERR_ARG, "bad motif");
+  const dm::MotifTable t = dm::table_of(g, motif);
+  if (!t.d_toff) return dm::fail(DM_ERR_ARG, "motif table not built");
+  dm::DeviceGuard dg(g->device);
+  if (rows_out && t.rows > 0) {
+    std::vector<int32_t> buf((size_t)t.rows * t.stride);
+    DM_CUDA(cudaMemcpy(buf.data(), t.d_rows, sizeof(int32_t) * buf.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < t.rows; ++i)
+      std::memcpy(rows_out + i * t.L, buf.data() + i * t.stride, sizeof(int32_t) * (size_t)t.L);
+  }
+  if (toff_out) DM_CUDA(cudaMemcpy(toff_out, t.d_toff, sizeof(int64_t) * ((size_t)g->arcs + 1), cudaMemcpyDeviceToHost));
   return DM_OK;
 }
 
