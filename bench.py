@@ -62,6 +62,13 @@ WORKLOADS = {
 }
 
 
+# Topology-aware motif sets (§6.3: "motif selection should be topology-aware"): for the
+# heavy-hex P30 workload a long path motif (Res(M7), built once by Alg. 2 as data preparation)
+# gives the fewest materialized levels and a 6-vertex table tail (measured sets);
+# the other workloads keep the implicit {M2, M3, M3-O}.
+MOTIFS = {"c5": "M2,M7", "c3-p20": "M2,M7"}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -185,6 +192,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--motifs", default=None,
+                    help="planner motif set (MOTIF_SETS name or comma list, e.g. M2,M7); default: the "
+                         "workload's topology-aware set (MOTIFS below)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--rebalance", type=int, default=-1,
@@ -220,12 +230,17 @@ def main():
     desc, gfn, pfn, drop = WORKLOADS[args.workload]
     n, e = gfn()
     k, pe = pfn()
+    motifs = args.motifs or MOTIFS.get(args.workload, "all")
 
     stream = torch.cuda.current_stream()
     t0 = time.perf_counter()
     G = dm.Graph(n, e, drop_self_loops=drop, device=local)
     prep_s = time.perf_counter() - t0
-    plan = G.plan(k, pe)                     # the plan dm_match executes (dm_plan_create_for)
+    t0 = time.perf_counter()
+    db = G.build_motifs(motifs, stream=stream)   # Alg. 2 motif database (data preparation)
+    torch.cuda.synchronize()
+    prep_db_s = time.perf_counter() - t0
+    plan = G.plan(k, pe, motifs=motifs)      # the plan dm_match executes (dm_plan_create_for)
     cuts = plan.seed_cuts(G, world)          # equal-work seed ranges (library)
     seed = (cuts[rank], cuts[rank + 1])
     flush = torch.empty(int(300e6) // 4, dtype=torch.int32, device="cuda")  # > 126 MB L2
@@ -247,12 +262,12 @@ def main():
 
     def one(profile=False):
         if dist_on and rebalance_step > 0:
-            fr = G.match_prefix(k, pe, rebalance_step, seed_range=seed, stream=stream)
+            fr = G.match_prefix(k, pe, rebalance_step, seed_range=seed, stream=stream, motifs=motifs)
             mine = rebalance_rows(fr.rows_tensor(), fr.work_tensor(), fr.work_total, rank=rank,
                                   world=world, coll_device=torch.device(coll_dev), stream=stream)
-            r = G.match_resume(k, pe, rebalance_step, mine, stream=stream, profile=profile)
+            r = G.match_resume(k, pe, rebalance_step, mine, stream=stream, profile=profile, motifs=motifs)
         else:
-            r = G.match(k, pe, seed_range=seed, stream=stream, profile=profile)
+            r = G.match(k, pe, seed_range=seed, stream=stream, profile=profile, motifs=motifs)
         # C3: the job's count, all_reduced inside the timed step
         total = reduce_count(r.count, coll_device=torch.device(coll_dev)) if dist_on else r.count
         return r, total
@@ -263,10 +278,11 @@ def main():
     # cold query (after the warm-up, so kernels are loaded): the first dm_match on a freshly created graph (no growth-ratio cache, so every
     # level size is read back before the next step is launched), device-timed
     Gc = dm.Graph(n, e, drop_self_loops=drop, device=local)
+    Gc.build_motifs(motifs, stream=stream)
     barrier()
     ca, cb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ca.record(stream)
-    rc = Gc.match(k, pe, seed_range=seed, stream=stream)
+    rc = Gc.match(k, pe, seed_range=seed, stream=stream, motifs=motifs)
     cb.record(stream)
     barrier()
     cold_ms = ca.elapsed_time(cb)
@@ -377,15 +393,16 @@ def main():
         epin = pin.numpy()
         for _ in range(2):
             G2 = dm.Graph(n, epin, drop_self_loops=drop, device=local)
-            G2.match(k, pe, seed_range=seed, stream=stream)
+            G2.match(k, pe, seed_range=seed, stream=stream, motifs=motifs)
             G2.close()
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
         ecount = 0
         for _ in range(args.e2e_steps):
+            # public API, cold: graph build + motif database (lazily, inside the first match) + match
             G2 = dm.Graph(n, epin, drop_self_loops=drop, device=local)
-            r2 = G2.match(k, pe, seed_range=seed, stream=stream)
+            r2 = G2.match(k, pe, seed_range=seed, stream=stream, motifs=motifs)
             ecount += r2.count
             G2.close()
         b.record(stream)
@@ -417,7 +434,10 @@ def main():
                "config": {"workload": desc, "embeddings_per_step": int(total_count / args.steps),
                           "data_graph_vertices": n, "data_graph_edges": int(len(e)),
                           "pattern_vertices": k, "mode": "count (monomorphism)",
-                          "motifs": "M3-O,M3,M2", "plan_steps": plan.num_steps,
+                          "motifs": motifs, "plan_steps": plan.num_steps,
+                          "plan": [st.get("table") or len(st.get("new", [])) for st in plan.describe()["steps"]],
+                          "motif_db": {kk: {"rows": v[0], "build_ms": v[1]} for kk, v in db.items()},
+                          "prep_ms_motif_db": prep_db_s * 1e3,
                           "l2_flush": "300 MB buffer written between timed steps",
                           "parallelism": f"seed-shard x{world} (replicated graph)" +
                           (f", all-to-all frontier rebalance at level {rebalance_step}"

@@ -59,7 +59,8 @@ typedef enum {
   DM_ERR_OOM = -5,                  /* device or host allocation failed                    */
   DM_ERR_ROW_BUDGET = -6,           /* table mode: result larger than row_budget   */
   DM_ERR_CUDA = -7,                 /* CUDA runtime error / no device                      */
-  DM_ERR_UNSUPPORTED = -8           /* k > DM_MAX_PATTERN, ...                             */
+  DM_ERR_UNSUPPORTED = -8,          /* k > DM_MAX_PATTERN, ...                             */
+  DM_ERR_IO = -9                    /* motif database file missing / unreadable / corrupt  */
 } dm_status;
 
 enum { DM_MONO = 0, DM_INDUCED = 1 };                      /* isomorphism variant (DESIGN Q1) */
@@ -172,6 +173,19 @@ DM_API dm_status dm_graph_build_motifs(dm_graph *g, int32_t motifs, const dm_mat
 DM_API int64_t dm_graph_motif_rows(const dm_graph *g, int32_t motif);
 DM_API double dm_graph_motif_build_ms(const dm_graph *g, int32_t motif);
 DM_API dm_status dm_graph_motif_table(const dm_graph *g, int32_t motif, int32_t *rows_out, int64_t *toff_out);
+/*
+ * Motif database persistence (SPEC save_database / load_database; the "performed
+ * once, cached, and reused" preparation of P:336-338): dm_graph_save_motifs writes every built
+ * Res(M) table of g to one file (atomically: path.tmp then rename); dm_graph_load_motifs adds the
+ * file's tables to g without rebuilding them.  The file is bound to the graph by a fingerprint
+ * (FNV-1a over n and the sorted, deduplicated CSR = an order-independent hash of the edge set);
+ * every table carries a checksum.
+ * Errors: DM_ERR_IO (cannot open / write, bad magic or version, truncated file, checksum
+ * mismatch), DM_ERR_ARG (fingerprint mismatch: the file was built for another graph), DM_ERR_OOM,
+ * DM_ERR_CUDA.  Tables already resident in g are kept.
+ */
+DM_API dm_status dm_graph_save_motifs(const dm_graph *g, const char *path);
+DM_API dm_status dm_graph_load_motifs(dm_graph *g, const char *path);
 /* Device pointers of the CSR (owned by g, valid until dm_graph_destroy). */
 DM_API dm_status dm_graph_device_csr(const dm_graph *g, const int64_t **d_off, const int32_t **d_adj);
 /* Copy the CSR to host buffers off_out[n+1] and adj_out[num_arcs] (either may be NULL). */
@@ -297,6 +311,26 @@ DM_API dm_status dm_rows_partition_by_key(const int32_t *d_rows, int64_t n, int3
                                           const int32_t *splitters, int32_t parts, int32_t *d_out,
                                           int64_t *counts, void *stream);
 DM_API dm_status dm_table_sort(int32_t *d_rows, int64_t n, int32_t k, int32_t n_vertices, void *stream);
+
+/*
+ * dm_score_layouts -- layout generation + scoring + ranking (quantum layout selection, PAPER.md
+ * §6.5; SPEC layout-scoring S:472-508): every embedding f of the pattern in g (as
+ * dm_match in table mode with opt's mode / motif set), scored
+ *     score(f) = prod_{v in V_p} node_fid[f(v)] * prod_{(a,b) in p_edges} edge_fid(f(a), f(b))
+ * in float64 (vertex factors in pattern-vertex order, then the edges in the given order), and
+ * the top_k rows by descending score, ties in ascending lexicographic row order.
+ *   node_fid   HOST double[n], each in (0, 1]
+ *   fid_edges  HOST int32[fm][2] undirected data edges, fid_vals HOST double[fm] in (0, 1]; every
+ *              data edge needs a fidelity (duplicates: the last one wins)
+ *   rows_out   HOST int32[top_k][k], scores_out HOST double[top_k]; *n_out = min(top_k, count),
+ *              *count_out (may be NULL) = number of layouts
+ * Errors: DM_ERR_ARG (top_k <= 0, fidelity outside (0, 1], fidelity for a non-edge, a data edge
+ * without fidelity), DM_ERR_VERTEX_RANGE, plus dm_match's.  Synchronous on opt->cuda_stream.
+ */
+DM_API dm_status dm_score_layouts(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                                  const double *node_fid, const int32_t *fid_edges, const double *fid_vals,
+                                  int64_t fm, const dm_match_opts *opt, int64_t top_k, int32_t *rows_out,
+                                  double *scores_out, int64_t *n_out, uint64_t *count_out);
 
 /* Thread-local message of the last failing call on this thread ("" if none). */
 DM_API const char *dm_last_error(void);

@@ -24,7 +24,7 @@ LIB_PATH = os.path.join(_HERE, "libdeltamotif.so")
 DM_OK = 0
 ERRORS = {-1: "DM_ERR_ARG", -2: "DM_ERR_VERTEX_RANGE", -3: "DM_ERR_SELF_LOOP",
           -4: "DM_ERR_PATTERN_DISCONNECTED", -5: "DM_ERR_OOM", -6: "DM_ERR_ROW_BUDGET",
-          -7: "DM_ERR_CUDA", -8: "DM_ERR_UNSUPPORTED"}
+          -7: "DM_ERR_CUDA", -8: "DM_ERR_UNSUPPORTED", -9: "DM_ERR_IO"}
 DM_MONO, DM_INDUCED = 0, 1
 DM_OUT_COUNT, DM_OUT_TABLE = 1, 2
 DM_MOTIF_M2, DM_MOTIF_M3, DM_MOTIF_M3O = 1, 2, 4
@@ -94,7 +94,8 @@ EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_
            "dm_plan_width", "dm_plan_stride", "dm_plan_column_vertex", "dm_plan_seed_work",
            "dm_plan_seed_cuts", "dm_plan_seed", "dm_plan_step", "dm_plan_finish_table", "dm_plan_run",
            "dm_rows_partition_by_work", "dm_rows_partition_by_key", "dm_table_sort",
-           "dm_graph_build_motifs", "dm_graph_motif_rows", "dm_graph_motif_build_ms", "dm_graph_motif_table"]
+           "dm_graph_build_motifs", "dm_graph_motif_rows", "dm_graph_motif_build_ms", "dm_graph_motif_table",
+           "dm_graph_save_motifs", "dm_graph_load_motifs", "dm_score_layouts"]
 
 
 def lib():
@@ -170,6 +171,10 @@ def lib():
         "dm_graph_motif_rows": (c.c_int64, [P, c.c_int32]),
         "dm_graph_motif_build_ms": (c.c_double, [P, c.c_int32]),
         "dm_graph_motif_table": (c.c_int, [P, c.c_int32, P, P]),
+        "dm_graph_save_motifs": (c.c_int, [P, c.c_char_p]),
+        "dm_graph_load_motifs": (c.c_int, [P, c.c_char_p]),
+        "dm_score_layouts": (c.c_int, [P, c.c_int32, P, c.c_int64, P, P, P, c.c_int64, c.POINTER(_Opts),
+                                       c.c_int64, P, P, c.POINTER(c.c_int64), c.POINTER(c.c_uint64)]),
     }
     for name, (rt, args) in sig.items():
         f = getattr(L, name)
@@ -512,6 +517,14 @@ class Graph:
         return {MOTIF_NAMES[b]: (self.motif_rows(b), lib().dm_graph_motif_build_ms(self._h, b))
                 for b in MOTIF_NAMES if b >= 8 and bits & b}
 
+    def save_motifs(self, path: str):
+        """dm_graph_save_motifs: persist the built motif tables (fingerprinted)."""
+        _check(lib().dm_graph_save_motifs(self._h, os.fsencode(path)))
+
+    def load_motifs(self, path: str):
+        """dm_graph_load_motifs: add the tables of a saved database (fingerprint-checked)."""
+        _check(lib().dm_graph_load_motifs(self._h, os.fsencode(path)))
+
     def motif_rows(self, motif) -> int:
         b = MOTIF_BITS[motif] if isinstance(motif, str) else int(motif)
         return int(lib().dm_graph_motif_rows(self._h, b))
@@ -607,6 +620,28 @@ class Graph:
             return Result(cnt, rows, _stats_dict(st))
         finally:
             L.dm_result_free(r)
+
+    def score_layouts(self, k: int, p_edges, node_fid, fid_edges, fid_vals, top_k: int, *,
+                      mode: str = "mono", motifs="all", stream=None):
+        """dm_score_layouts: the top_k layouts (embeddings) by fidelity score (§6.5).
+        Returns (rows [m][k] int32, scores [m] float64, total number of layouts)."""
+        pe = _edges_arr(p_edges)
+        nf = np.ascontiguousarray(np.asarray(node_fid, dtype=np.float64))
+        fe = _edges_arr(fid_edges)
+        fv = np.ascontiguousarray(np.asarray(fid_vals, dtype=np.float64).reshape(-1))
+        if nf.shape != (self.n,) or fv.shape[0] != fe.shape[0]:
+            raise ValueError("node_fid must have n entries and fid_vals one per fidelity edge")
+        o = self._opts(mode, "table", motifs, None, stream, False, 0, 0)
+        m = max(int(top_k), 1)
+        rows = np.zeros((m, k), dtype=np.int32)
+        scores = np.zeros(m, dtype=np.float64)
+        n_out, cnt = ctypes.c_int64(0), ctypes.c_uint64(0)
+        _check(lib().dm_score_layouts(self._h, int(k), pe.ctypes.data if pe.size else None, pe.shape[0],
+                                      nf.ctypes.data, fe.ctypes.data if fe.size else None,
+                                      fv.ctypes.data if fv.size else None, fe.shape[0], ctypes.byref(o),
+                                      int(top_k), rows.ctypes.data, scores.ctypes.data, ctypes.byref(n_out),
+                                      ctypes.byref(cnt)))
+        return rows[: n_out.value], scores[: n_out.value], int(cnt.value)
 
     def match(self, k: int, p_edges, *, mode: str = "mono", output: str = "count",
               motifs="all", seed_range=None, stream=None, profile: bool = False,

@@ -159,6 +159,11 @@ cudaError_t launch_agg_to_excl(const unsigned long long *agg, int64_t tiles, uin
 
 DevStep make_dev_step(const Step &st);
 
+// canonical match table [count][k] on the device (match.cu); *d_table is allocated with
+// cudaMallocAsync on opt's stream (free it with cudaFreeAsync / cudaFree), NULL when count == 0
+dm_status match_device_table(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                             const dm_match_opts *opt, int32_t **d_table, uint64_t *count);
+
 // ---- table steps (tabstep.cu): one slice's fresh vertices joined with Res(M) (Step::tab_motif)
 struct DevTabStep {
   int32_t in_w, n_new;

@@ -1009,7 +1009,9 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     c.st.probes[i] = slot_sum(2 * kAccSlots + 2 * kAccSlots * i);
     const bool lastc = (i + 1 == plan.steps.size()) && !c.table;
     const double rin = (double)c.st.rows_in[i], rout = (double)c.st.rows_out[i];
-    const double lookups = 8.0 * rin + 4.0 * (double)c.st.candidates[i] + 4.0 * (double)c.st.probes[i];
+    // a table step's candidate is a Res(M) row: its n_new new ids are read (4 B each)
+    const double cand_ids = plan.steps[i].tab_motif ? (double)plan.steps[i].n_new : 1.0;
+    const double lookups = 8.0 * rin + 4.0 * cand_ids * (double)c.st.candidates[i] + 4.0 * (double)c.st.probes[i];
     // SURVEY §8(d) as written: 4 B per id, the seed's one-column input included
     c.st.bytes_model[i] = 4.0 * (double)c.st.width_in[i] * rin + lookups +
                           (lastc ? 0.0 : 4.0 * (double)c.st.width_out[i] * rout);
@@ -1063,6 +1065,31 @@ dm_status build_motif_table(const dm_graph *g, int id, cudaStream_t s, uint64_t 
   t.build_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return st;
 }
+
+}  // namespace
+
+// The canonical table of a match on the device (library-owned buffer handed to the caller,
+// cudaFree): the layout-scoring path ranks it without a host round trip.
+dm_status match_device_table(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
+                             const dm_match_opts *opt, int32_t **d_table, uint64_t *count) {
+  dm_match_opts o;
+  dm_match_opts_init(&o);
+  if (opt) o = *opt;
+  o.output = DM_OUT_TABLE;
+  RunSpec rs;
+  rs.no_host_table = true;
+  int32_t *tab = nullptr;
+  rs.d_canon_owned = &tab;
+  dm_result *r = nullptr;
+  dm_status st = match_impl(g, k, p_edges, pm, &o, &r, rs);
+  if (st != DM_OK) return st;
+  *count = r->count;
+  *d_table = tab;
+  dm_result_free(r);
+  return DM_OK;
+}
+
+namespace {
 
 dm_status make_frontier(const dm_graph *g, const dm_match_opts *opt, const FrontierOut &fo, dm_frontier **out) {
   dm_frontier *f = new (std::nothrow) dm_frontier;

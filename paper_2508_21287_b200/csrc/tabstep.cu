@@ -70,7 +70,8 @@ __device__ __forceinline__ int32_t tcomp(const int4 (&E)[3], int p) {
 
 constexpr int kWarpStage = 64;  // survivors staged per warp before a warp-level flush
 // per-row 512-bit membership filter of the row's vertex set (one hash; ~5% false positives for
-// 24-column rows, against ~17% for a 128-bit filter); stride 17 words (bank spread)
+// 24-column rows, against ~17% for a 128-bit filter; 1024 bits measured slower: the larger
+// shared-memory footprint costs a CTA per SM); stride 17 words (bank spread)
 constexpr int kFiltWords = 16, kFiltStride = 17;
 __device__ __forceinline__ uint32_t filt_hash(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) >> 23; }
 
@@ -149,8 +150,7 @@ __global__ void __launch_bounds__(kStepThreads)
         }
       }
     }
-    s_meta[tid] = make_int4((int)lo, (int)seg1, (int)seg2, row[w - 1]);
-    f[kFiltWords] = (uint32_t)(w >= 2 ? row[w - 2] : -1);  // the filter row's spare word
+    s_meta[tid] = make_int4((int)lo, (int)seg1, (int)seg2, 0);
     cnt = tot;
   }
   long long incl = cnt;
@@ -196,7 +196,6 @@ __global__ void __launch_bounds__(kStepThreads)
 #pragma unroll
     for (int i = 0; i < 3; ++i) E[i] = i < NE ? __ldg(ent + i) : make_int4(-1, -1, -1, -1);
     const uint32_t *f = filt + r * kFiltStride;
-    const int32_t t0 = meta.w, t1 = (int32_t)f[kFiltWords];
     bool ok = true;
     if (eqmask) {  // further bound template positions: the remaining join constraints
 #pragma unroll
@@ -207,11 +206,9 @@ __global__ void __launch_bounds__(kStepThreads)
 #pragma unroll
     for (int p = 0; p < TS; ++p) {
       if ((newmask >> p) & 1u) {
-        // all-distinct: not one of the row's last two columns; the 512-bit row filter
-        // sends the few possible duplicates to the exact scan below
-        const int32_t x = tcomp(E, p);
-        ok = ok && x != t0 && x != t1;
-        const uint32_t h = filt_hash(x);
+        // all-distinct: the row filter sends the few possible duplicates to the exact
+        // scan below
+        const uint32_t h = filt_hash(tcomp(E, p));
         hits |= ((f[h >> 5] >> (h & 31)) & 1u) << p;
       }
     }

@@ -61,7 +61,7 @@ def _check_plan(dm, k, pe, motifs, mode="mono"):
     padj = np.zeros((k, k), bool)
     for a, b in np.asarray(pe).reshape(-1, 2).tolist():
         padj[a, b] = padj[b, a] = True
-    tmpl = {"M2": [(0, 1)], "M3": [(0, 1), (1, 2)], "M3-O": [(0, 1), (1, 2), (0, 2)]}
+    tmpl = _templates()
     covered = set()
     union = set()
     for i, s in enumerate(P.slices()):
@@ -81,8 +81,35 @@ def _check_plan(dm, k, pe, motifs, mode="mono"):
     cols = d["col_pvert"]
     assert sorted(cols) == list(range(k)) and cols[0] == P.first_vertex
     enforced, nonenf = [], []
+    slices = P.slices()
     for st in d["steps"]:
-        assert 1 <= len(st["new"]) <= 2
+        if "table" in st:   # table step: one slice's fresh vertices from Res(M) (Alg. 1 l.6)
+            w = st["in_w"]
+            T = slices[st["slice"]]
+            assert T["motif"] == st["table"]
+            pos = {0: cols[st["key0"]]}
+            if st["key1"] >= 0:
+                pos[1] = cols[st["key1"]]
+            for p, c in st["eq"]:
+                assert c < w
+                pos[p] = cols[c]
+            for j, p in enumerate(st["newpos"]):
+                pos[p] = cols[w + j]
+            L = len(T["vertices"])
+            assert sorted(pos) == list(range(L)) and sorted(pos.values()) == sorted(T["vertices"])
+            assert st["key0"] < w and all(c < w for c in [st["key1"]] if c >= 0)
+            newv = {cols[w + j] for j in range(st["n_new"])}
+            for a, b in tmpl[st["table"]]:   # the template maps onto pattern edges
+                assert padj[pos[a], pos[b]]
+                if pos[a] in newv or pos[b] in newv:
+                    enforced.append(tuple(sorted((pos[a], pos[b]))))
+            for j, c, neg in st["probes"]:
+                assert c < w + j
+                (nonenf if neg else enforced).append(tuple(sorted((cols[c], cols[w + j]))))
+            if mode == "induced":   # non-edges inside the slice are probed too
+                pass
+            continue
+        assert 1 <= len(st["new"]) <= 4
         w = st["in_w"]
         for j, nv in enumerate(st["new"]):
             col = w + j
@@ -100,6 +127,50 @@ def _check_plan(dm, k, pe, motifs, mode="mono"):
     else:
         assert not nonenf
     return P, d
+
+
+def _templates():
+    t = {"M2": [(0, 1)], "M3": [(0, 1), (1, 2)], "M3-O": [(0, 1), (1, 2), (0, 2)]}
+    for L in (4, 5, 6, 7, 8):
+        t[f"M{L}"] = [(i, i + 1) for i in range(L - 1)]
+    for L in (4, 6, 12):
+        t[f"M{L}-O"] = [(i, i + 1) for i in range(L - 1)] + [(L - 1, 0)]
+    return t
+
+
+TABLE_SETS = ["heavy-hex", "grid", "M2,M5", "M2,M3,M6", "M2,M7", "M2,M3,M8", "M2,M12-O",
+              "M2,M3,M3-O,M4,M5,M6,M7,M8,M4-O,M6-O,M12-O"]
+
+
+@pytest.mark.parametrize("motifs", TABLE_SETS)
+@pytest.mark.parametrize("mode", ["mono", "induced"])
+def test_plan_table_motifs_valid(dm, motifs, mode):
+    """Decompositions with the larger motifs and their table steps: every
+    template maps onto pattern edges, full edge coverage, every pattern edge enforced
+    exactly once (by a Res(M) template edge of the step that places it, or a probe), every
+    non-edge probed in induced mode."""
+    rng = np.random.default_rng(11)
+    cases = [g.path(30), g.ring(12), g.ring(6), g.path(7)]
+    for lat in (g.ibm_heavy_hex(6), g.grid(12), g.hex_lattice_subdivided(3, 4)):
+        for sz in (8, 14, 25):
+            k, pe, _ = g.random_connected_subgraph(*lat, sz, int(rng.integers(0, 1 << 30)))
+            cases.append((k, pe))
+    for k, pe in cases:
+        _check_plan(dm, k, pe, motifs, mode=mode)
+
+
+def test_plan_table2_sizes_fast(dm):
+    """100-vertex random subgraphs of the paper's lattices plan in well under a
+    second with every motif set (the decomposition is <1% of the runtime)."""
+    import time
+    for lat, sets in ((g.hex_lattice_subdivided(25, 34), ("all", "heavy-hex")), (g.grid(60), ("all", "grid"))):
+        for seed in (1, 2):
+            k, pe, _ = g.random_connected_subgraph(*lat, 100, seed)
+            for m in sets:
+                t = time.perf_counter()
+                P = dm.Plan(k, pe, motifs=m)
+                assert time.perf_counter() - t < 1.0
+                assert P.width(P.num_steps) == 100
 
 
 def test_plan_paths_use_wedge_chain(dm):

@@ -114,3 +114,42 @@ def test_config5_random_subgraphs_motif_sets(dm):
         for motifs in ("heavy-hex", "M2,M3,M6", "M2,M12-O"):
             r = G.match(k, pe, output="both", motifs=motifs)
             assert np.array_equal(r.rows, o.rows), (s, motifs)
+
+
+def test_motif_db_save_load(dm, tmp_path):
+    """Motif-database persistence: save -> load into a fresh graph built
+    from the same edge set in another order gives bit-identical tables (no rebuild) and the same
+    results; another graph -> fingerprint error; truncated / corrupted file -> DM_ERR_IO."""
+    n, e = g.ibm_heavy_hex(10)
+    G = dm.Graph(n, e)
+    info = G.build_motifs("M2,M5,M7,M6-O,M12-O")
+    path = str(tmp_path / "hh10.dmdb")
+    G.save_motifs(path)
+    G2 = dm.Graph(n, e[::-1, ::-1].copy())
+    G2.load_motifs(path)
+    for m in ("M5", "M7", "M6-O", "M12-O"):
+        a, b = G.motif_table(m), G2.motif_table(m)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and info[m][0] == len(b[0])
+        assert dm.lib().dm_graph_motif_build_ms(G2._h, dm.MOTIF_BITS[m]) == 0.0   # loaded, not built
+    want = oracle.match(n, e, *g.path(20), table=False).count
+    assert G2.match(*g.path(20), motifs="M2,M7").count == want
+    G3 = dm.Graph(*g.ibm_heavy_hex(6))
+    with pytest.raises(dm.DMError) as ei:
+        G3.load_motifs(path)
+    assert ei.value.code == -1 and "fingerprint" in str(ei.value)
+    data = open(path, "rb").read()
+    bad = str(tmp_path / "trunc.dmdb")
+    open(bad, "wb").write(data[: len(data) // 2])
+    G4 = dm.Graph(n, e)
+    with pytest.raises(dm.DMError) as ei:
+        G4.load_motifs(bad)
+    assert ei.value.code == -9
+    flip = bytearray(data)
+    flip[len(flip) // 2] ^= 0xFF
+    open(bad, "wb").write(bytes(flip))
+    with pytest.raises(dm.DMError) as ei:
+        G4.load_motifs(bad)
+    assert ei.value.code == -9
+    with pytest.raises(dm.DMError) as ei:
+        G4.load_motifs(str(tmp_path / "missing.dmdb"))
+    assert ei.value.code == -9
