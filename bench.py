@@ -66,7 +66,9 @@ WORKLOADS = {
 # heavy-hex P30 workload a long path motif (Res(M7), built once by Alg. 2 as data preparation)
 # gives the fewest materialized levels and a 6-vertex table tail (measured sets);
 # the other workloads keep the implicit {M2, M3, M3-O}.
-MOTIFS = {"c5": "M2,M7", "c3-p20": "M2,M7"}
+MOTIFS = {"c5": "M2,M7", "c3-p20": "M2,M7",
+          # 4-clique on R-MAT: the triangle-apex table feeds the shared-key pair step
+          "c4-k4": "apex", "c4-k4-s16": "apex"}
 
 
 def load_peaks():

@@ -41,7 +41,7 @@ extern "C" {
 #define DM_API
 #endif
 
-#define DM_ABI_VERSION 3
+#define DM_ABI_VERSION 4
 #define DM_MAX_PATTERN 128 /* max pattern vertices k (the paper's Table 2 goes to 100) */
 
 typedef struct dm_graph dm_graph;   /* device CSR of G_d (Res(M2), both orientations) */
@@ -74,11 +74,17 @@ enum { DM_OUT_COUNT = 1, DM_OUT_TABLE = 2 };               /* output bit flags  
 enum {
   DM_MOTIF_M2 = 1, DM_MOTIF_M3 = 2, DM_MOTIF_M3O = 4,
   DM_MOTIF_M4 = 8, DM_MOTIF_M5 = 16, DM_MOTIF_M6 = 32, DM_MOTIF_M7 = 64, DM_MOTIF_M8 = 128,
-  DM_MOTIF_M4O = 256, DM_MOTIF_M6O = 512, DM_MOTIF_M12O = 1024
+  DM_MOTIF_M4O = 256, DM_MOTIF_M6O = 512, DM_MOTIF_M12O = 1024,
+  /* Res(M3-O) materialized as the triangle-apex table keyed by directed edge (
+   * P:262, Alg. 2): apex(a,b) = N(a) ∩ N(b) for every arc.  Not a decomposition motif
+   * (the planner keeps M3-O implicit); when it is in the set, shared-key pair steps on arc rows
+   * (diamond, 4-clique) take both new vertices' candidates from it (dm_graph_apex_table). */
+  DM_MOTIF_APEX = 2048
 };
 #define DM_MOTIF_IMPLICIT (DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O)
 #define DM_MOTIF_TABLES (DM_MOTIF_M4 | DM_MOTIF_M5 | DM_MOTIF_M6 | DM_MOTIF_M7 | DM_MOTIF_M8 | \
                          DM_MOTIF_M4O | DM_MOTIF_M6O | DM_MOTIF_M12O)
+#define DM_MOTIF_ALL (DM_MOTIF_IMPLICIT | DM_MOTIF_TABLES | DM_MOTIF_APEX)
 #define DM_MAX_MOTIF_VERTICES 12
 enum { DM_GRAPH_DROP_SELF_LOOPS = 1 };                     /* dm_graph_create flags           */
 enum { DM_MATCH_PROFILE = 1 };                             /* dm_match_opts.flags: time every
@@ -173,6 +179,21 @@ DM_API dm_status dm_graph_build_motifs(dm_graph *g, int32_t motifs, const dm_mat
 DM_API int64_t dm_graph_motif_rows(const dm_graph *g, int32_t motif);
 DM_API double dm_graph_motif_build_ms(const dm_graph *g, int32_t motif);
 DM_API dm_status dm_graph_motif_table(const dm_graph *g, int32_t motif, int32_t *rows_out, int64_t *toff_out);
+/*
+ * Triangle-apex table (Res(M3-O) of P:262 keyed by directed edge, built once
+ * per graph like the Alg. 2 tables): dm_graph_build_motifs(g, DM_MOTIF_APEX, opt)
+ * builds it on the device (two-pass: per-arc |N(a) ∩ N(b)|, exclusive scan, write).
+ *   dm_graph_apex_entries: total entries (= 6 x #triangles = tr(A^3)), -1 if not built.
+ *   dm_graph_apex_build_ms: host wall time of the build, -1 if not built.
+ *   dm_graph_apex_table: copy to HOST toff_out[num_arcs + 1] (int64 offsets: arc e = (a, adj[e])
+ *       owns entries [toff[e], toff[e+1])) and/or apex_out[entries]: each entry is the CSR arc
+ *       index of (a, c) for c in N(a) ∩ N(b), ascending (vertex c = adj[entry]).  Either may be NULL.
+ * Errors: DM_ERR_ARG (not built), DM_ERR_CUDA; the build: DM_ERR_UNSUPPORTED (>= 2^31 arcs),
+ * DM_ERR_OOM, DM_ERR_CUDA.
+ */
+DM_API int64_t dm_graph_apex_entries(const dm_graph *g);
+DM_API double dm_graph_apex_build_ms(const dm_graph *g);
+DM_API dm_status dm_graph_apex_table(const dm_graph *g, int64_t *toff_out, int32_t *apex_out);
 /*
  * Motif database persistence (SPEC save_database / load_database; the "performed
  * once, cached, and reused" preparation of P:336-338): dm_graph_save_motifs writes every built

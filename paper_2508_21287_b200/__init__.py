@@ -29,14 +29,15 @@ DM_MONO, DM_INDUCED = 0, 1
 DM_OUT_COUNT, DM_OUT_TABLE = 1, 2
 DM_MOTIF_M2, DM_MOTIF_M3, DM_MOTIF_M3O = 1, 2, 4
 MOTIF_BITS = {"M2": 1, "M3": 2, "M3-O": 4, "M4": 8, "M5": 16, "M6": 32, "M7": 64, "M8": 128,
-              "M4-O": 256, "M6-O": 512, "M12-O": 1024}
+              "M4-O": 256, "M6-O": 512, "M12-O": 1024, "apex": 2048}
 MOTIF_NAMES = {v: k for k, v in MOTIF_BITS.items()}
 DM_MAX_MOTIF_VERTICES = 12
 DM_GRAPH_DROP_SELF_LOOPS = 1
 DM_MATCH_PROFILE = 1
 DM_MAX_PATTERN = 128
 DM_MAX_STEPS = 128
-ABI_VERSION = 3
+ABI_VERSION = 4
+DM_MOTIF_APEX = 2048
 
 MOTIF_SETS = {
     "all": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O,   # the implicit (CSR-joined) motifs
@@ -46,6 +47,8 @@ MOTIF_SETS = {
     # the paper's topology-aware sets: heavy-hex {M2, M4}, square grid {M2, M4-O, M6-O}
     "heavy-hex": DM_MOTIF_M2 | 8,
     "grid": DM_MOTIF_M2 | 256 | 512,
+    # implicit motifs + the triangle-apex table (Res(M3-O) keyed by arc) for pair steps
+    "apex": DM_MOTIF_M2 | DM_MOTIF_M3 | DM_MOTIF_M3O | 2048,
 }
 
 
@@ -95,7 +98,8 @@ EXPORTS = ["dm_match_opts_init", "dm_abi_version", "dm_graph_create", "dm_graph_
            "dm_plan_seed_cuts", "dm_plan_seed", "dm_plan_step", "dm_plan_finish_table", "dm_plan_run",
            "dm_rows_partition_by_work", "dm_rows_partition_by_key", "dm_table_sort",
            "dm_graph_build_motifs", "dm_graph_motif_rows", "dm_graph_motif_build_ms", "dm_graph_motif_table",
-           "dm_graph_save_motifs", "dm_graph_load_motifs", "dm_score_layouts"]
+           "dm_graph_save_motifs", "dm_graph_load_motifs", "dm_score_layouts",
+           "dm_graph_apex_entries", "dm_graph_apex_build_ms", "dm_graph_apex_table"]
 
 
 def lib():
@@ -172,6 +176,9 @@ def lib():
         "dm_graph_motif_build_ms": (c.c_double, [P, c.c_int32]),
         "dm_graph_motif_table": (c.c_int, [P, c.c_int32, P, P]),
         "dm_graph_save_motifs": (c.c_int, [P, c.c_char_p]),
+        "dm_graph_apex_entries": (c.c_int64, [P]),
+        "dm_graph_apex_build_ms": (c.c_double, [P]),
+        "dm_graph_apex_table": (c.c_int, [P, P, P]),
         "dm_graph_load_motifs": (c.c_int, [P, c.c_char_p]),
         "dm_score_layouts": (c.c_int, [P, c.c_int32, P, c.c_int64, P, P, P, c.c_int64, c.POINTER(_Opts),
                                        c.c_int64, P, P, c.POINTER(c.c_int64), c.POINTER(c.c_uint64)]),
@@ -514,8 +521,22 @@ class Graph:
         bits = _motifs(motifs)
         o = self._opts("mono", "count", bits, None, stream, False, 0, row_budget)
         _check(lib().dm_graph_build_motifs(self._h, bits, ctypes.byref(o)))
-        return {MOTIF_NAMES[b]: (self.motif_rows(b), lib().dm_graph_motif_build_ms(self._h, b))
-                for b in MOTIF_NAMES if b >= 8 and bits & b}
+        out = {MOTIF_NAMES[b]: (self.motif_rows(b), lib().dm_graph_motif_build_ms(self._h, b))
+               for b in MOTIF_NAMES if 8 <= b < DM_MOTIF_APEX and bits & b}
+        if bits & DM_MOTIF_APEX:
+            out["apex"] = (int(lib().dm_graph_apex_entries(self._h)), lib().dm_graph_apex_build_ms(self._h))
+        return out
+
+    def apex_table(self):
+        """(toff [num_arcs + 1] int64, apex [entries] int32 arc indices) of the built triangle-apex
+        table (dm_graph_apex_table, host copies)."""
+        ne = int(lib().dm_graph_apex_entries(self._h))
+        if ne < 0:
+            raise DMError(-1, "triangle-apex table not built")
+        toff = np.empty(self.num_arcs + 1, dtype=np.int64)
+        apex = np.empty(max(ne, 1), dtype=np.int32)
+        _check(lib().dm_graph_apex_table(self._h, toff.ctypes.data, apex.ctypes.data))
+        return toff, apex[:ne]
 
     def save_motifs(self, path: str):
         """dm_graph_save_motifs: persist the built motif tables (fingerprinted)."""

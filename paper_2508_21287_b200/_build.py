@@ -9,7 +9,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdeltamotif.so")
-SOURCES = ["errors.cpp", "planner.cpp", "graph.cu", "extend.cu", "tail.cu", "pairs.cu", "exchange.cu", "tabstep.cu", "motifdb.cu", "scoring.cu", "match.cu"]
+SOURCES = ["errors.cpp", "planner.cpp", "graph.cu", "extend.cu", "tail.cu", "pairs.cu", "apex.cu", "exchange.cu", "tabstep.cu", "motifdb.cu", "scoring.cu", "match.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",

@@ -25,9 +25,19 @@ struct MotifTable {
   int64_t *d_toff = nullptr;  // [arcs + 1]
   double build_ms = 0.0;
 };
+// The triangle-apex table (apex.cu): Res(M3-O) keyed by directed edge --
+// apex(a,b) = N(a) ∩ N(b) of CSR arc e = (a,b) is d_apex[d_toff[e] .. d_toff[e+1]), each entry
+// the arc index of (a, c) (its vertex is adj[entry]), ascending.
+struct ApexTable {
+  int64_t *d_toff = nullptr;  // [arcs + 1]
+  int32_t *d_apex = nullptr;  // [entries]
+  int64_t entries = -1;       // -1: not built
+  double build_ms = 0.0;
+};
 struct TabStore {
   std::mutex mu;
   MotifTable t[32];  // by motif bit index
+  ApexTable apex;
 };
 int motif_bit(int id);  // bit index of a DM_MOTIF_* id
 }  // namespace dm
@@ -150,6 +160,11 @@ int pair_mode_of(const DevStep &st);
 bool row_serial_step(const DevStep &st, const dm_graph &g);
 cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g, int pair_mode,
                          cudaStream_t s);
+// shared-key pair step on the triangle-apex table (apex.cu)
+dm_status build_apex_table(const dm_graph *g, cudaStream_t s, ApexTable &t);
+bool apex_pair_step(const DevStep &st, int elem);
+cudaError_t launch_pairs_apex(const DevStep &st, const StepIO &io, const dm_graph &g, const ApexTable &t,
+                              cudaStream_t s);
 // deep count-only last step (3..kMaxNew new vertices) on ELL graphs (tail.cu: k_deep)
 cudaError_t launch_tail(const DevStep &st, const StepIO &io, const dm_graph &g, int64_t tiles,
                         cudaStream_t s);

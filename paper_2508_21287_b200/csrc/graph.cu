@@ -287,6 +287,8 @@ void dm_graph_destroy(dm_graph *g) {
       cudaFree(t.d_rows);
       cudaFree(t.d_toff);
     }
+    cudaFree(g->tabs->apex.d_toff);
+    cudaFree(g->tabs->apex.d_apex);
     delete g->tabs;
   }
   cudaFree(g->d_off);

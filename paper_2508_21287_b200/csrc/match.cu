@@ -152,6 +152,7 @@ struct Ctx {
   std::vector<DevStep> dsteps;
   std::vector<DevTabStep> tsteps;       // table steps (Step::tab_motif != 0), by step index
   std::vector<MotifTable> tabs;         //   ... and the motif table each one joins with
+  ApexTable apex;                       // triangle-apex table (a1b) when the motif set asks for it
   unsigned long long *d_acc = nullptr;  // [slots] count-mode total, then per step i:
                                         //   [C_i slots][Q_i slots] (kAccSlots each)
   int32_t *d_res = nullptr;             // table mode: rows in column (match) order
@@ -185,6 +186,7 @@ cudaError_t launch_count_step(const Ctx &c, int si, const StepIO &io, int64_t ti
   if (is_tab(c, si)) return launch_table(kModeCount, c.tsteps[(size_t)si], io, *c.g, c.tabs[(size_t)si], tiles, c.s);
   const DevStep &D = c.dsteps[(size_t)si];
   const int pm = pair_mode_of(D);
+  if (pm >= 0 && c.apex.d_toff && apex_pair_step(D, io.elem)) return launch_pairs_apex(D, io, *c.g, c.apex, c.s);
   if (pm >= 0 && !row_serial_step(D, *c.g)) return launch_pairs(D, io, *c.g, pm, c.s);
   return launch_step_count(D, io, *c.g, tiles, c.s);
 }
@@ -689,8 +691,14 @@ dm_status build_motif_table(const dm_graph *g, int id, cudaStream_t s, uint64_t 
 
 // Builds the missing tables of `motifs` (thread-safe; built tables are immutable).
 dm_status ensure_tables(const dm_graph *g, int motifs, cudaStream_t s, uint64_t row_budget) {
-  if (!(motifs & DM_MOTIF_TABLES)) return DM_OK;
+  if (!(motifs & (DM_MOTIF_TABLES | DM_MOTIF_APEX))) return DM_OK;
   std::lock_guard<std::mutex> lk(g->tabs->mu);
+  if ((motifs & DM_MOTIF_APEX) && g->tabs->apex.entries < 0) {
+    ApexTable at;
+    dm_status st = build_apex_table(g, s, at);
+    if (st != DM_OK) return st;
+    g->tabs->apex = at;
+  }
   for (const MotifDef *M : motif_defs()) {
     if (!(motifs & M->id) || !motif_is_table(M->id)) continue;
     MotifTable &t = g->tabs->t[motif_bit(M->id)];
@@ -712,6 +720,11 @@ dm_status ensure_tables_on(const dm_graph *g, const dm_match_opts &o) {
 MotifTable table_of(const dm_graph *g, int id) {
   std::lock_guard<std::mutex> lk(g->tabs->mu);
   return g->tabs->t[motif_bit(id)];
+}
+
+ApexTable apex_of(const dm_graph *g) {
+  std::lock_guard<std::mutex> lk(g->tabs->mu);
+  return g->tabs->apex;
 }
 
 PlanStats graph_plan_stats(const dm_graph *g, bool count_only, int motifs) {
@@ -830,6 +843,10 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
     }
     c.tabs.push_back(t);
     c.tsteps.push_back(s.tab_motif ? make_dev_tab_step(s, t) : DevTabStep{});
+  }
+  if (plan.motifs & DM_MOTIF_APEX) {
+    c.apex = apex_of(g);
+    if (c.apex.entries < 0) return fail(DM_ERR_ARG, "plan uses the triangle-apex table this graph has not built");
   }
   c.ratio.assign(plan.steps.size(), 0.0);
   for (size_t i = 0; i < plan.steps.size(); ++i) {
@@ -1320,7 +1337,7 @@ dm_status dm_plan_finish_table(const dm_graph *g, const dm_plan *p, const dm_mat
 dm_status dm_graph_build_motifs(dm_graph *g, int32_t motifs, const dm_match_opts *opt) {
   dm::clear_error();
   if (!g) return dm::fail(DM_ERR_ARG, "graph is NULL");
-  if (motifs & ~(DM_MOTIF_IMPLICIT | DM_MOTIF_TABLES)) return dm::fail(DM_ERR_ARG, "unknown motif bit");
+  if (motifs & ~DM_MOTIF_ALL) return dm::fail(DM_ERR_ARG, "unknown motif bit");
   dm_match_opts o;
   dm_match_opts_init(&o);
   if (opt) o = *opt;
@@ -1353,6 +1370,30 @@ dm_status dm_graph_motif_table(const dm_graph *g, int32_t motif, int32_t *rows_o
       std::memcpy(rows_out + i * t.L, buf.data() + i * t.stride, sizeof(int32_t) * (size_t)t.L);
   }
   if (toff_out) DM_CUDA(cudaMemcpy(toff_out, t.d_toff, sizeof(int64_t) * ((size_t)g->arcs + 1), cudaMemcpyDeviceToHost));
+  return DM_OK;
+}
+
+int64_t dm_graph_apex_entries(const dm_graph *g) {
+  if (!g) return -1;
+  return dm::apex_of(g).entries;
+}
+
+double dm_graph_apex_build_ms(const dm_graph *g) {
+  if (!g) return -1.0;
+  const dm::ApexTable t = dm::apex_of(g);
+  return t.entries < 0 ? -1.0 : t.build_ms;
+}
+
+dm_status dm_graph_apex_table(const dm_graph *g, int64_t *toff_out, int32_t *apex_out) {
+  dm::clear_error();
+  if (!g) return dm::fail(DM_ERR_ARG, "graph is NULL");
+  const dm::ApexTable t = dm::apex_of(g);
+  if (t.entries < 0) return dm::fail(DM_ERR_ARG, "triangle-apex table not built");
+  dm::DeviceGuard dg(g->device);
+  if (!dg.ok) return dm::fail(DM_ERR_CUDA, "cudaSetDevice failed");
+  if (toff_out) DM_CUDA(cudaMemcpy(toff_out, t.d_toff, sizeof(int64_t) * ((size_t)g->arcs + 1), cudaMemcpyDeviceToHost));
+  if (apex_out && t.entries > 0)
+    DM_CUDA(cudaMemcpy(apex_out, t.d_apex, sizeof(int32_t) * (size_t)t.entries, cudaMemcpyDeviceToHost));
   return DM_OK;
 }
 

@@ -381,7 +381,7 @@ dm_status build_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t moti
   if (k > DM_MAX_PATTERN) return fail(DM_ERR_UNSUPPORTED, "pattern larger than DM_MAX_PATTERN");
   if (pm < 0 || (pm > 0 && !p_edges)) return fail(DM_ERR_ARG, "bad pattern edge list");
   if (mode != DM_MONO && mode != DM_INDUCED) return fail(DM_ERR_ARG, "mode must be DM_MONO or DM_INDUCED");
-  if (motifs & ~(DM_MOTIF_IMPLICIT | DM_MOTIF_TABLES)) return fail(DM_ERR_ARG, "unknown motif bit");
+  if (motifs & ~DM_MOTIF_ALL) return fail(DM_ERR_ARG, "unknown motif bit");
   Pat P{k, std::vector<std::vector<char>>(k, std::vector<char>(k, 0))};
   for (int64_t i = 0; i < pm; ++i) {
     int a = p_edges[2 * i], b = p_edges[2 * i + 1];
@@ -406,7 +406,7 @@ dm_status build_plan(int32_t k, const int32_t *p_edges, int64_t pm, int32_t moti
   Plan plan;
   plan.k = k;
   plan.mode = mode;
-  plan.motifs = (motifs & (DM_MOTIF_IMPLICIT | DM_MOTIF_TABLES)) | DM_MOTIF_M2;
+  plan.motifs = (motifs & DM_MOTIF_ALL) | DM_MOTIF_M2;
   for (int a = 0; a < k; ++a)
     for (int b = a + 1; b < k; ++b)
       if (P.adj[a][b]) plan.edges.push_back({a, b});

@@ -14,7 +14,7 @@ tot_t = 0.0
 for (i, k), m in per.items():
     t = m.get("gpu__time_duration.sum", 0.0)
     tot_t += t
-    mk = re.search(r"k_(?:rows|step)<(\d)", k)
+    mk = re.search(r"k_(?:rows|step|table)<(\d)", k)
     if "k_pairs" in k or "k_deep" in k:
         kind = "join_count"
     elif mk:
