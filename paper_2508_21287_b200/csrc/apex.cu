@@ -88,14 +88,17 @@ __global__ void __launch_bounds__(kApexThreads)
 // columns, so the first new vertex's candidate set is exactly S = apex(u, v) (u = the endpoint
 // of lower degree) -- the equi-join on two keys becomes one table lookup.  The pair
 // (x0, x1), x0, x1 in S, passes injectivity iff x0 != x1 (S holds neither u nor v: no
-// self-loops); with the closing edge (x0, x1) (4-clique, MODE 1) x1 must lie in
+// self-loops); with the closing edge (x0, x1) (4-clique) x1 must lie in
 // S ∩ N(x0) = S ∩ apex(u, x0): both are position sets in N(u), so S is put in a per-warp
 // bitmap over N(u) and every entry of apex(u, x0) is one bit test.  Entries of the apex lists of
 // 32 consecutive x0 are spread over the lanes as one flat range (segment found by a shuffle
 // bisection over the lanes' exclusive prefix), so short and long lists keep all lanes busy.
-// MODE 0 (pairs only distinct, diamond): |S| (|S| - 1) per row -- the size of the pair join
-// (S x S minus its diagonal).  MODE 2 (induced non-edge): |S| (|S| - 1) - #edges.
-template <int MODE>
+// This is the join of x1 on the keys {u, x0} (Res(M3-O) again) with the closing edge (x1, v) as
+// the probe -- a re-association of the pair step, every candidate of that join is
+// inspected, and injectivity holds by construction (x1 is in N(u) ∩ N(x0) ∩ N(v), no self-loops).
+// Only the closing-edge pair step (4-clique) uses it: the distinct-pairs (diamond) and induced
+// non-edge pair steps keep pairs.cu, which inspects every pair of S (no count-mode
+// shortcut that skips inspecting candidates).
 __global__ void __launch_bounds__(kStepThreads)
     k_pairs_apex(const StepIO io_, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
                  const int64_t *__restrict__ toff, const int32_t *__restrict__ apex,
@@ -107,7 +110,7 @@ __global__ void __launch_bounds__(kStepThreads)
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
   const int64_t wg = (int64_t)blockIdx.x * kWarps + wl;
   uint32_t *B = gbits ? gbits + wg * (int64_t)bm_words : s_bits + wl * bm_words;
-  if (MODE != 0 && !gbits) {
+  if (!gbits) {
     for (int i = lane; i < bm_words; i += 32) B[i] = 0u;
     __syncwarp();
   }
@@ -126,10 +129,7 @@ __global__ void __launch_bounds__(kStepThreads)
       const int64_t e = lower_bound_g(adj, lu, hu, v);  // arc (u, v): every lane, broadcast loads
       const int64_t s0 = __ldg(toff + e), ns = __ldg(toff + e + 1) - s0;
       if (lane == 0) cand += (unsigned long long)ns;
-      if (MODE == 0 || ns < 2) {
-        if (lane == 0) cnt += (unsigned long long)(ns * (ns - 1));
-        continue;
-      }
+      if (ns < 2) continue;
       for (int64_t i = lane; i < ns; i += 32) {
         const int64_t p = __ldg(apex + s0 + i) - lu;
         atomicOr(B + (p >> 5), 1u << (p & 31));
@@ -176,8 +176,7 @@ __global__ void __launch_bounds__(kStepThreads)
         B[p >> 5] = 0u;
       }
       __syncwarp();
-      if (MODE == 1) cnt += edges;
-      else cnt += (lane == 0 ? (unsigned long long)(ns * (ns - 1)) : 0ull) - edges;
+      cnt += edges;
     }
   }
   cand += probes;  // second-level candidates: the apex entries inspected
@@ -258,18 +257,17 @@ bool apex_pair_step(const DevStep &st, int elem) {
   if (st.in_w != 2 || st.n_new != 2 || elem != 4) return false;
   if (st.n_nbr[0] != 2 || st.n_non[0] != 0) return false;
   const bool keys = (st.nbr[0][0] == 0 && st.nbr[0][1] == 1) || (st.nbr[0][0] == 1 && st.nbr[0][1] == 0);
-  return keys && pair_mode_of(st) >= 0;
+  return keys && pair_mode_of(st) == 1;
 }
 
 cudaError_t launch_pairs_apex(const DevStep &st, const StepIO &io, const dm_graph &g, const ApexTable &t,
                               cudaStream_t s) {
   if (io.in_rows <= 0 && !io.d_in_rows) return cudaSuccess;
-  const int mode = pair_mode_of(st);
   const int bm_words = (g.max_deg + 31) / 32 + 1;
   const size_t smem = sizeof(uint32_t) * (size_t)bm_words * (kStepThreads / 32);
-  const bool use_smem = mode == 0 || smem <= 160 * 1024;
-  auto kern = mode == 0 ? k_pairs_apex<0> : mode == 1 ? k_pairs_apex<1> : k_pairs_apex<2>;
-  const size_t dyn = (use_smem && mode != 0) ? smem : 0;
+  const bool use_smem = smem <= 160 * 1024;
+  auto kern = k_pairs_apex;
+  const size_t dyn = use_smem ? smem : 0;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
   if (e != cudaSuccess) return e;
   int per_sm = 0, sms = 0, dev = 0;

@@ -2,8 +2,11 @@
 paper's lattices whose embedding count keeps the CPU oracle within seconds.  Many
 random-walk subgraphs of lattices are trees with 1e7-1e8 labelled embeddings (the oracle needs
 minutes for those), so seeds are screened with a root-sampled oracle estimate and then counted
-exactly.  Calls only oracle/ and dm_inputs; writes tests/golden/table2_seeds.json."""
+exactly; an exact count that does not finish within TIMEOUT seconds drops the seed.  Calls only
+oracle/ and dm_inputs; writes tests/golden/table2_seeds.json.  Usage: pick_table2_seeds.py [lattice ...]
+(default: all; results of other lattices already in the file are kept)."""
 import json
+import multiprocessing as mp
 import os
 import sys
 
@@ -14,8 +17,32 @@ import oracle  # noqa: E402
 LATTICES = {"hex11x33": lambda: g.hex_lattice_subdivided(11, 33), "hex25x34": lambda: g.hex_lattice_subdivided(25, 34),
             "grid40": lambda: g.grid(40), "grid60": lambda: g.grid(60)}
 LIMIT = {20: 2_000_000, 40: 2_000_000, 60: 2_000_000, 80: 20_000_000, 100: 20_000_000}
-out = {}
+TIMEOUT = 90
+PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden", "table2_seeds.json")
+
+
+def _count(args, q):
+    n, e, k, pe = args
+    q.put(oracle.match(n, e, k, pe, table=False).count)
+
+
+def exact_count(n, e, k, pe):
+    q = mp.Queue()
+    pr = mp.Process(target=_count, args=((n, e, k, pe), q))
+    pr.start()
+    pr.join(TIMEOUT)
+    if pr.is_alive():
+        pr.kill()
+        pr.join()
+        return None
+    return q.get()
+
+
+out = json.load(open(PATH))["seeds"] if os.path.exists(PATH) else {}
+todo = sys.argv[1:] or list(LATTICES)
 for name, fn in LATTICES.items():
+    if name not in todo:
+        continue
     n, e = fn()
     for size, lim in LIMIT.items():
         picked = []
@@ -27,10 +54,10 @@ for name, fn in LATTICES.items():
             est = oracle.match(n, e, k, pe, table=False, roots=(0, R)).count * (n / R)
             if est > 3 * lim:
                 continue
-            c = oracle.match(n, e, k, pe, table=False).count
-            if c <= lim:
+            c = exact_count(n, e, k, pe)
+            if c is not None and c <= lim:
                 picked.append([seed, int(c)])
         out[f"{name}/{size}"] = picked
         print(name, size, picked, flush=True)
-json.dump({"source": "scripts/pick_table2_seeds.py (oracle counts; P:437-443 workload shape)", "seeds": out},
-          open(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "table2_seeds.json"), "w"), indent=1)
+        json.dump({"source": "scripts/pick_table2_seeds.py (oracle counts; P:437-443 workload shape)", "seeds": out},
+                  open(PATH, "w"), indent=1)
