@@ -244,6 +244,12 @@ __global__ void __launch_bounds__(kStepThreads)
     const int per = io.out_elem == 2 ? 8 : 4;
     const int c0 = per * q;
     const bool all_parent = c0 + per <= w;
+    // aligned tail: when the output columns from the last chunk boundary before w (w_al) to the
+    // row end fit the TS staged words, a survivor is staged as exactly those columns (parent
+    // columns [w_al, w), then the new vertices in output order), so a flush lane whose chunk
+    // reaches past w reads its chunk with 16-byte loads -- no per-column source selection
+    const int w_al = (w / per) * per;
+    const bool tail_fast = Wn - w_al <= TS;
     unsigned long long codes = 0;
     for (int i = 0; i < per; ++i) {
       const int c = c0 + i;
@@ -292,10 +298,18 @@ __global__ void __launch_bounds__(kStepThreads)
           int32_t v[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
           if (!all_parent) {
             const int32_t *nv = sv_new + o * TS;
+            if (tail_fast) {  // the staged tail holds this chunk's columns at offset c0 - w_al
+              const int4 ta = *reinterpret_cast<const int4 *>(nv + (c0 - w_al));
+              const int4 tb = per == 8 ? *reinterpret_cast<const int4 *>(nv + (c0 - w_al) + 4) : neg;
+              const int32_t t[8] = {ta.x, ta.y, ta.z, ta.w, tb.x, tb.y, tb.z, tb.w};
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const unsigned code = (unsigned)(codes >> (8 * i)) & 0xFFu;
-              if (code != 0xFEu) v[i] = code == 0xFFu ? -1 : nv[code];
+              for (int i = 0; i < 8; ++i) v[i] = c0 + i < Wn ? t[i] : -1;
+            } else {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const unsigned code = (unsigned)(codes >> (8 * i)) & 0xFFu;
+                if (code != 0xFEu) v[i] = code == 0xFFu ? -1 : nv[code];
+              }
             }
           }
           if (io.out_elem == 2) {
@@ -323,9 +337,11 @@ __global__ void __launch_bounds__(kStepThreads)
         const int slot = fill + __popc(m & lt);
         stage_r[slot] = r;
         int32_t *nv = sv_new + slot * TS;
+        const int nb = tail_fast ? w - w_al : 0;  // aligned tail: parent columns [w_al, w) first
+        for (int c = 0; c < nb; ++c) nv[c] = rows[r * ss + w_al + c];
 #pragma unroll
         for (int p = 0; p < TS; ++p)
-          if ((newmask >> p) & 1u) nv[st.colpos[p]] = tcomp(E, p);
+          if ((newmask >> p) & 1u) nv[nb + st.colpos[p]] = tcomp(E, p);
       }
       fill += __popc(m);
       if (fill > kWarpStage - 32) {
