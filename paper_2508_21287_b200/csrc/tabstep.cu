@@ -75,11 +75,54 @@ constexpr int kWarpStage = 64;  // survivors staged per warp before a warp-level
 constexpr int kFiltWords = 16, kFiltStride = 17;
 __device__ __forceinline__ uint32_t filt_hash(int32_t v) { return ((uint32_t)v * 0x9E3779B1u) >> 23; }
 
+// 16-bit levels (R16): the tile is kept in shared memory as the stored uint16 ids (half the bytes
+// of widened rows: more CTAs per SM), rows padded to an odd number of 16-byte chunks
+// (conflict-free LDS.128 across lanes); the exact all-distinct scan compares two ids per 32-bit
+// word (__vcmpeq2; padding 0xFFFF is never an id since n <= 65535).
+__host__ __device__ inline int smem_stride16(int w) {
+  const int rs = row_stride16(w);
+  return ((rs >> 3) & 1) ? rs : rs + 8;
+}
+__device__ __forceinline__ bool in_row16(const uint16_t *row, int nq8, int32_t x) {
+  const uint32_t xx = (uint32_t)x * 0x10001u;
+  const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
+  uint32_t hit = 0;
+  for (int q = 0; q < nq8; ++q) {
+    const uint4 v = r4[q];
+    hit |= __vcmpeq2(v.x, xx) | __vcmpeq2(v.y, xx) | __vcmpeq2(v.z, xx) | __vcmpeq2(v.w, xx);
+  }
+  return hit != 0u;
+}
+// tile of 16-bit rows -> shared memory (no widening): one TMA bulk copy when the smem stride
+// equals the stored stride, else 16-byte chunks.  Ends with a CTA barrier.
+__device__ __forceinline__ void load_tile16(uint16_t *rows, int ss16, int rs16, const StepIO &io, int64_t r0,
+                                            int nrows, uint64_t *bar) {
+  const uint16_t *src = reinterpret_cast<const uint16_t *>(io.in) + r0 * rs16;
+  if (ss16 == rs16) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar, 1);
+      const unsigned bytes = (unsigned)(nrows * rs16) * 2u;
+      mbar_expect_tx(bar, bytes);
+      tma_bulk_g2s(rows, src, bytes, bar);
+    }
+    __syncthreads();
+    mbar_wait(bar, 0);
+    return;
+  }
+  const int nq8 = rs16 >> 3, total = nrows * nq8;
+  const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+  for (int i = threadIdx.x; i < total; i += kStepThreads) {
+    const int r = i / nq8, q = i - r * nq8;
+    reinterpret_cast<uint4 *>(rows + r * ss16)[q] = __ldcs(s4 + i);
+  }
+  __syncthreads();
+}
+
 // Warp-level join: warp w owns the tile rows [32w, 32w+32) (lane = row for the index lookups);
 // the warp's entries are laid out by a warp scan of the per-row entry counts and inspected 32 per
 // round, lane -> entry, the entry's row found by a 5-step shuffle bisection of the row offsets.
 // No CTA barrier between the tile load and the epilogue.  TS = table row stride (4, 8 or 12 ids).
-template <int MODE, bool ELL, int TS>
+template <int MODE, bool ELL, int TS, bool R16>
 __global__ void __launch_bounds__(kStepThreads)
     k_table(const DevTabStep st, const StepIO io_, const int64_t *__restrict__ off,
             const int32_t *__restrict__ adj, const int32_t *__restrict__ tab,
@@ -95,7 +138,9 @@ __global__ void __launch_bounds__(kStepThreads)
   constexpr int kWarps = kStepThreads / 32;
   constexpr int NE = TS / 4;  // int4 loads per table row
 
-  const int w = st.in_w, ws = row_stride(w), ss = smem_stride(w);
+  // ss: smem row stride in elements (int32, or uint16 for R16); ws: int32 words of a widened row
+  const int w = st.in_w, ws = row_stride(w), ss = R16 ? smem_stride16(w) : smem_stride(w);
+  const int nq8 = row_stride16(w) >> 3;  // R16: 16-byte chunks of a stored row
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   int64_t tile;
   if (MODE == kModeSingle) {
@@ -109,28 +154,38 @@ __global__ void __launch_bounds__(kStepThreads)
   if (r0 >= io.in_rows) return;
   const int nrows = (int)(io.in_rows - r0 < kTileRows ? io.in_rows - r0 : kTileRows);
   int32_t *rows = reinterpret_cast<int32_t *>(smem_raw);
-  uint32_t *filt = reinterpret_cast<uint32_t *>(rows + kTileRows * ss);  // [kTileRows][kFiltStride]
+  uint16_t *rows16 = reinterpret_cast<uint16_t *>(smem_raw);
+  uint32_t *filt = reinterpret_cast<uint32_t *>(smem_raw + (size_t)kTileRows * ss * (R16 ? 2 : 4));  // [kTileRows][kFiltStride]
   int32_t *sv_new = reinterpret_cast<int32_t *>(filt + kTileRows * kFiltStride) + warp * kWarpStage * TS;
   int32_t *stage_r = reinterpret_cast<int32_t *>(filt + kTileRows * kFiltStride) + kWarps * kWarpStage * TS +
                      warp * kWarpStage;
-  load_tile(rows, ss, ws, io, r0, nrows, &s_bar);  // ends with a CTA barrier
+  if constexpr (R16) load_tile16(rows16, ss, row_stride16(w), io, r0, nrows, &s_bar);  // ends with a CTA barrier
+  else load_tile(rows, ss, ws, io, r0, nrows, &s_bar);
   const int4 *ell = reinterpret_cast<const int4 *>(io.ell);
+  // column c (< w) of tile row r
+  auto RV = [&](int r, int c) -> int32_t {
+    if constexpr (R16) return (int32_t)rows16[r * ss + c];
+    else return rows[r * ss + c];
+  };
+  auto IN_ROW = [&](int r, int32_t x) -> bool {
+    if constexpr (R16) return in_row16(rows16 + r * ss, nq8, x);
+    else return in_row(rows + r * ss, ws, x);
+  };
 
   // ---- lane = row: index range(s) of the join and the row's membership filter
   long long cnt = 0;
   if (tid < nrows) {
-    const int32_t *row = rows + tid * ss;
     uint32_t *f = filt + tid * kFiltStride;
 #pragma unroll
     for (int i = 0; i < kFiltWords; ++i) f[i] = 0u;
     for (int c = 0; c < w; ++c) {
-      const uint32_t h = filt_hash(row[c]);
+      const uint32_t h = filt_hash(RV(tid, c));
       f[h >> 5] |= 1u << (h & 31);
     }
-    const int32_t a = row[st.key0];
+    const int32_t a = RV(tid, st.key0);
     long long lo = 0, seg1 = 0, seg2 = 0, tot = 0;
     if (st.key1 >= 0) {
-      const int64_t ai = arc_index<ELL>(off, adj, ell, a, row[st.key1]);
+      const int64_t ai = arc_index<ELL>(off, adj, ell, a, RV(tid, st.key1));
       if (ai >= 0) {
         lo = __ldg(toff + ai);
         seg1 = tot = __ldg(toff + ai + 1) - lo;
@@ -141,7 +196,7 @@ __global__ void __launch_bounds__(kStepThreads)
       seg1 = tot = hi - lo;
       seg2 = hi;
       if (st.skip >= 0) {
-        const int64_t ai = arc_index<ELL>(off, adj, ell, a, row[st.skip]);
+        const int64_t ai = arc_index<ELL>(off, adj, ell, a, RV(tid, st.skip));
         if (ai >= 0) {
           const long long slo = __ldg(toff + ai), shi = __ldg(toff + ai + 1);
           seg1 = slo - lo;
@@ -191,7 +246,6 @@ __global__ void __launch_bounds__(kStepThreads)
     const int4 meta = s_meta[r];
     const int ei = loc < meta.y ? meta.x + loc : meta.z + (loc - meta.y);
     ++my_cand;
-    const int32_t *row = rows + r * ss;
     const int4 *ent = reinterpret_cast<const int4 *>(tab + (int64_t)ei * TS);
 #pragma unroll
     for (int i = 0; i < 3; ++i) E[i] = i < NE ? __ldg(ent + i) : make_int4(-1, -1, -1, -1);
@@ -200,7 +254,7 @@ __global__ void __launch_bounds__(kStepThreads)
     if (eqmask) {  // further bound template positions: the remaining join constraints
 #pragma unroll
       for (int p = 0; p < TS; ++p)
-        if ((eqmask >> p) & 1u) ok = ok && tcomp(E, p) == row[st.eq_colp[p]];
+        if ((eqmask >> p) & 1u) ok = ok && tcomp(E, p) == RV(r, st.eq_colp[p]);
     }
     uint32_t hits = 0;  // new positions whose filter bit is set: exact scan needed
 #pragma unroll
@@ -215,11 +269,11 @@ __global__ void __launch_bounds__(kStepThreads)
     while (ok && hits) {  // deferred exact scans: only the filter hits
       const int p = __ffs(hits) - 1;
       hits &= hits - 1;
-      if (in_row(row, ws, tsel(E, p))) ok = false;
+      if (IN_ROW(r, tsel(E, p))) ok = false;
     }
     for (int p = 0; p < st.n_pr && ok; ++p) {
       const int cc = st.pr_c[p];
-      const int32_t u = cc < w ? row[cc] : tsel(E, st.newpos[cc - w]);
+      const int32_t u = cc < w ? RV(r, cc) : tsel(E, st.newpos[cc - w]);
       const int32_t x = tsel(E, st.newpos[st.pr_j[p]]);
       ++my_probe;
       ok = edge_probe<ELL>(off, adj, ell, u, x) != (st.pr_neg[p] != 0);
@@ -291,11 +345,24 @@ __global__ void __launch_bounds__(kStepThreads)
       __syncwarp();
       if (base != ~0ull && q < nq) {
         for (int o = sub; o < fill; o += rpi) {
-          const int32_t *prow = rows + stage_r[o] * ss;
+          const int pr = stage_r[o];
           const int4 neg = make_int4(-1, -1, -1, -1);
-          const int4 pa = c0 < ws ? *reinterpret_cast<const int4 *>(prow + c0) : neg;
-          const int4 pb = (per == 8 && c0 + 4 < ws) ? *reinterpret_cast<const int4 *>(prow + c0 + 4) : neg;
-          int32_t v[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+          if (R16 && io.out_elem == 2 && all_parent) {  // 16 parent bytes copied as they are stored
+            reinterpret_cast<uint4 *>(io.out)[(int64_t)(base + o) * nq + q] =
+                *reinterpret_cast<const uint4 *>(rows16 + pr * ss + c0);
+            continue;
+          }
+          int32_t v[8];
+          if constexpr (R16) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = (i < per && c0 + i < w) ? RV(pr, c0 + i) : -1;
+          } else {
+            const int32_t *prow = rows + pr * ss;
+            const int4 pa = c0 < ws ? *reinterpret_cast<const int4 *>(prow + c0) : neg;
+            const int4 pb = (per == 8 && c0 + 4 < ws) ? *reinterpret_cast<const int4 *>(prow + c0 + 4) : neg;
+            v[0] = pa.x; v[1] = pa.y; v[2] = pa.z; v[3] = pa.w;
+            v[4] = pb.x; v[5] = pb.y; v[6] = pb.z; v[7] = pb.w;
+          }
           if (!all_parent) {
             const int32_t *nv = sv_new + o * TS;
             if (tail_fast) {  // the staged tail holds this chunk's columns at offset c0 - w_al
@@ -338,7 +405,7 @@ __global__ void __launch_bounds__(kStepThreads)
         stage_r[slot] = r;
         int32_t *nv = sv_new + slot * TS;
         const int nb = tail_fast ? w - w_al : 0;  // aligned tail: parent columns [w_al, w) first
-        for (int c = 0; c < nb; ++c) nv[c] = rows[r * ss + w_al + c];
+        for (int c = 0; c < nb; ++c) nv[c] = RV(r, w_al + c);
 #pragma unroll
         for (int p = 0; p < TS; ++p)
           if ((newmask >> p) & 1u) nv[nb + st.colpos[p]] = tcomp(E, p);
@@ -432,17 +499,19 @@ DevTabStep make_dev_tab_step(const Step &s, const MotifTable &t) {
   return d;
 }
 
-template <int MODE, bool ELL>
+template <int MODE, bool ELL, bool R16>
 cudaError_t launch_table_ts(const DevTabStep &st, const StepIO &io, const dm_graph &g, const MotifTable &t,
                             int64_t num_tiles, cudaStream_t s) {
   void (*kern)(const DevTabStep, const StepIO, const int64_t *, const int32_t *, const int32_t *, const int64_t *);
   switch (t.stride) {
-    case 4: kern = k_table<MODE, ELL, 4>; break;
-    case 8: kern = k_table<MODE, ELL, 8>; break;
-    default: kern = k_table<MODE, ELL, 12>; break;
+    case 4: kern = k_table<MODE, ELL, 4, R16>; break;
+    case 8: kern = k_table<MODE, ELL, 8, R16>; break;
+    default: kern = k_table<MODE, ELL, 12, R16>; break;
   }
   const int TS = t.stride <= 4 ? 4 : (t.stride <= 8 ? 8 : 12);
-  const size_t smem = sizeof(int32_t) * (size_t)kTileRows * smem_stride(st.in_w) +
+  const size_t row_bytes = R16 ? sizeof(uint16_t) * (size_t)smem_stride16(st.in_w)
+                               : sizeof(int32_t) * (size_t)smem_stride(st.in_w);
+  const size_t smem = row_bytes * (size_t)kTileRows +
                       sizeof(uint32_t) * (size_t)kTileRows * kFiltStride +
                       (MODE != kModeCount ? sizeof(int32_t) * (size_t)(kStepThreads / 32) * kWarpStage * (TS + 1) : 0);
   cudaError_t e = prep((const void *)kern, 0, smem);
@@ -457,14 +526,16 @@ cudaError_t launch_table(int mode, const DevTabStep &st, const StepIO &io, const
   StepIO io2 = io;
   io2.ell = g.d_ell;
   const bool ell = g.d_ell != nullptr;
-  if (mode == kModeCount)
-    return ell ? launch_table_ts<kModeCount, true>(st, io2, g, t, num_tiles, s)
-               : launch_table_ts<kModeCount, false>(st, io2, g, t, num_tiles, s);
-  if (mode == kModeSingle)
-    return ell ? launch_table_ts<kModeSingle, true>(st, io2, g, t, num_tiles, s)
-               : launch_table_ts<kModeSingle, false>(st, io2, g, t, num_tiles, s);
-  return ell ? launch_table_ts<kModeWrite, true>(st, io2, g, t, num_tiles, s)
-             : launch_table_ts<kModeWrite, false>(st, io2, g, t, num_tiles, s);
+  const bool r16 = io.elem == 2 && io.in != nullptr;  // 16-bit level kept 16-bit in shared memory
+#define DM_TABLE_LAUNCH(M)                                                                   \
+  return ell ? (r16 ? launch_table_ts<M, true, true>(st, io2, g, t, num_tiles, s)           \
+                    : launch_table_ts<M, true, false>(st, io2, g, t, num_tiles, s))         \
+             : (r16 ? launch_table_ts<M, false, true>(st, io2, g, t, num_tiles, s)          \
+                    : launch_table_ts<M, false, false>(st, io2, g, t, num_tiles, s))
+  if (mode == kModeCount) DM_TABLE_LAUNCH(kModeCount);
+  if (mode == kModeSingle) DM_TABLE_LAUNCH(kModeSingle);
+  DM_TABLE_LAUNCH(kModeWrite);
+#undef DM_TABLE_LAUNCH
 }
 
 dm_status finish_motif_table(const dm_graph &g, int32_t *packed, int64_t rows, MotifTable &t, cudaStream_t s) {

@@ -44,21 +44,23 @@ def test_table2_tables(dm, lattice, size):
             assert r.count == o.count and np.array_equal(r.rows, o.rows), (lattice, size, seed, motifs)
         # the witness embedding is one of the rows
         assert (r.rows == wit).all(axis=1).any()
+    if size == 40:  # induced mode on one of them (the patterns are induced subgraphs of the lattice)
+        k, pe, _ = g.random_connected_subgraph(n, e, size, SEEDS[f"{lattice}/{size}"][0][0])
+        o = oracle.match(n, e, k, pe, induced=True)
+        r = G.match(k, pe, mode="induced", output="both", motifs=tset)
+        assert r.count == o.count and np.array_equal(r.rows, o.rows)
 
 
 @pytest.mark.parametrize("size", [80, 100])
 @pytest.mark.parametrize("lattice", list(LATTICES))
 def test_table2_counts_large_patterns(dm, lattice, size):
+    """80- and 100-vertex patterns (beyond the round-1 cap of 64): counts against the oracle's
+    counts stored by scripts/pick_table2_seeds.py (the oracle needs up to ~70 s per lattice here)."""
     gfn, tset = LATTICES[lattice]
     n, e = gfn()
     G = dm.Graph(n, e)
     for seed, want in SEEDS[f"{lattice}/{size}"]:
         k, pe, _ = g.random_connected_subgraph(n, e, size, seed)
-        o = oracle.match(n, e, k, pe, table=False)
-        assert o.count == want
+        assert k == size
         for motifs in ("all", tset):
-            assert G.match(k, pe, motifs=motifs).count == o.count, (lattice, size, seed, motifs)
-    # induced mode on one of them (the patterns are induced subgraphs of the lattice)
-    k, pe, _ = g.random_connected_subgraph(n, e, size, SEEDS[f"{lattice}/{size}"][0][0])
-    o = oracle.match(n, e, k, pe, table=False, induced=True)
-    assert G.match(k, pe, mode="induced", motifs=tset).count == o.count
+            assert G.match(k, pe, motifs=motifs).count == want, (lattice, size, seed, motifs)
