@@ -136,15 +136,18 @@ __global__ void __launch_bounds__(kStepThreads)
       }
       __syncwarp();
       unsigned long long edges = 0;
+      // chunks of 32 x0: the next chunk's arcs (u, x0) are loaded while this chunk is tested, and
+      // two 32-entry rounds are in flight at a time (the apex lists are mostly L2/HBM reads)
+      int32_t e_nxt = lane < ns ? __ldg(apex + s0 + lane) : -1;
       for (int64_t c0 = 0; c0 < ns; c0 += 32) {
-        const int64_t i = c0 + lane;
+        const int32_t e0 = e_nxt;  // arc (u, x0) of this lane's x0, -1 past the end
         int64_t t0 = 0;
         int len = 0;
-        if (i < ns) {
-          const int32_t e0 = __ldg(apex + s0 + i);  // arc (u, x0)
+        if (e0 >= 0) {
           t0 = __ldg(toff + e0);
           len = (int)(__ldg(toff + e0 + 1) - t0);
         }
+        e_nxt = c0 + 32 + lane < ns ? __ldg(apex + s0 + c0 + 32 + lane) : -1;
         int incl = len;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
@@ -154,20 +157,21 @@ __global__ void __launch_bounds__(kStepThreads)
         const int total = __shfl_sync(0xffffffffu, incl, 31);
         const int excl = incl - len;
         if (lane == 0) probes += (unsigned long long)total;
-        for (int j0 = 0; j0 < total; j0 += 32) {
-          const int j = j0 + lane;
-          int k = 0;  // last lane whose segment starts at or before j
+        for (int j0 = 0; j0 < total; j0 += 64) {
+          const int ja = j0 + lane, jb = j0 + 32 + lane;
+          int ka = 0, kb = 0;  // last lane whose segment starts at or before ja / jb
 #pragma unroll
           for (int sft = 16; sft >= 1; sft >>= 1) {
-            const int ex = __shfl_sync(0xffffffffu, excl, k + sft);
-            if (ex <= j) k += sft;
+            if (__shfl_sync(0xffffffffu, excl, ka + sft) <= ja) ka += sft;
+            if (__shfl_sync(0xffffffffu, excl, kb + sft) <= jb) kb += sft;
           }
-          const int64_t tk = __shfl_sync(0xffffffffu, t0, k);
-          const int ek = __shfl_sync(0xffffffffu, excl, k);
-          if (j < total) {
-            const int64_t q = __ldg(apex + tk + (j - ek)) - lu;
-            edges += (B[q >> 5] >> (q & 31)) & 1u;
-          }
+          const int64_t tka = __shfl_sync(0xffffffffu, t0, ka), tkb = __shfl_sync(0xffffffffu, t0, kb);
+          const int eka = __shfl_sync(0xffffffffu, excl, ka), ekb = __shfl_sync(0xffffffffu, excl, kb);
+          const bool va = ja < total, vb = jb < total;
+          const int64_t qa = (va ? __ldg(apex + tka + (ja - eka)) : lu) - lu;
+          const int64_t qb = (vb ? __ldg(apex + tkb + (jb - ekb)) : lu) - lu;
+          edges += va & ((B[qa >> 5] >> (qa & 31)) & 1u);
+          edges += vb & ((B[qb >> 5] >> (qb & 31)) & 1u);
         }
       }
       __syncwarp();
