@@ -130,8 +130,26 @@ class ClockSampler:
             for nm, v in zip(names, parts[3:7]):
                 if v.lower() == "active":
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sms)}
+        note = None
+        if not sms:  # timed region shorter than the 100 ms sampling period: one sample right after it
+            try:
+                ln = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                    timeout=10).stdout.strip()
+                parts = [p.strip() for p in ln.split(",")]
+                sms.append(float(parts[0]))
+                mx = float(parts[1])
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+                note = "timed region < 100 ms: one sample taken right after it"
+            except Exception:
+                pass
+        out = {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+               "reasons": sorted(reasons), "samples": len(sms)}
+        if note:
+            out["note"] = note
+        return out
 
 
 def cpu_baseline(n, e, k, pe, drop, target_s=12.0):
@@ -357,7 +375,17 @@ def main():
     traffic = traffic_all.get(dom)
     total_model = sum(sum(s["bytes_model"]) for s in stats)
     ms_launch = ms / max(1, launches)
-    roof = {"bound": "hbm", "kernel": dom + " (extend.cu / tail.cu / pairs.cu)", "achieved": achieved,
+    # which kernel the dominant kind is on this plan (last step = the count kind in count mode)
+    psteps = plan.describe()["steps"]
+    last_tab = bool(psteps and psteps[-1].get("table"))
+    mid_tab = any(st.get("table") for st in psteps[:-1])
+    if dom == "join_count":
+        kname = ("k_table (tabstep.cu)" if last_tab else
+                 "k_pairs_apex (apex.cu) / k_pairs (pairs.cu) / k_deep_split (tail.cu) / k_rows, k_step (extend.cu)"
+                 if "apex" in str(motifs) else "k_pairs (pairs.cu) / k_deep_split (tail.cu) / k_rows, k_step (extend.cu)")
+    else:
+        kname = "k_table (tabstep.cu)" if mid_tab else "k_rows / k_step (extend.cu)"
+    roof = {"bound": "hbm", "kernel": dom + ": " + kname, "achieved": achieved,
             "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic["bytes_per_launch"] if isinstance(traffic, dict) else traffic,
             "algorithmic_bytes_per_launch": byts / max(1, launches),

@@ -197,8 +197,8 @@ DM_API dm_status dm_graph_apex_table(const dm_graph *g, int64_t *toff_out, int32
 /*
  * Motif database persistence (SPEC save_database / load_database; the "performed
  * once, cached, and reused" preparation of P:336-338): dm_graph_save_motifs writes every built
- * Res(M) table of g to one file (atomically: path.tmp then rename); dm_graph_load_motifs adds the
- * file's tables to g without rebuilding them.  The file is bound to the graph by a fingerprint
+ * Res(M) table of g, and the triangle-apex table if built, to one file (atomically: path.tmp then
+ * rename); dm_graph_load_motifs adds the file's tables to g without rebuilding them.  The file is bound to the graph by a fingerprint
  * (FNV-1a over n and the sorted, deduplicated CSR = an order-independent hash of the edge set);
  * every table carries a checksum.
  * Errors: DM_ERR_IO (cannot open / write, bad magic or version, truncated file, checksum

@@ -8,6 +8,8 @@
 //            | int64 n | int64 arcs | uint64 graph fingerprint
 //   table  : int32 motif id | int32 L | int64 rows | int32[rows][L] rows (template order,
 //            lexicographic) | int64[arcs + 1] arc index | uint64 FNV-1a of the table payload
+//            (the triangle-apex table, id DM_MOTIF_APEX: L = 1, rows = entries, the payload is the
+//            entry array (arc indices) and toff)
 // The graph fingerprint is FNV-1a over (n, the CSR offsets, the sorted adjacency), i.e. a hash
 // of the sorted, deduplicated edge list plus the vertex count (order independent in the input).
 #include <cstdio>
@@ -84,6 +86,17 @@ dm_status dm_graph_save_motifs(const dm_graph *g, const char *path) {
     std::lock_guard<std::mutex> lk(g->tabs->mu);
     for (auto &t : g->tabs->t)
       if (t.d_toff) tabs.push_back(t);
+    const dm::ApexTable &ap = g->tabs->apex;
+    if (ap.entries >= 0) {  // written like a one-column table: rows = entries
+      dm::MotifTable t;
+      t.motif = DM_MOTIF_APEX;
+      t.L = 1;
+      t.stride = 1;
+      t.rows = ap.entries;
+      t.d_rows = ap.d_apex;
+      t.d_toff = ap.d_toff;
+      tabs.push_back(t);
+    }
   }
   const std::string tmp = std::string(path) + ".tmp";
   dm::File F;
@@ -102,9 +115,14 @@ dm_status dm_graph_save_motifs(const dm_graph *g, const char *path) {
       return dm::fail(DM_ERR_CUDA, "D2H motif table");
     if (cudaMemcpy(toff.data(), t.d_toff, sizeof(int64_t) * toff.size(), cudaMemcpyDeviceToHost) != cudaSuccess)
       return dm::fail(DM_ERR_CUDA, "D2H motif index");
-    std::vector<int32_t> packed((size_t)t.rows * t.L);
-    for (int64_t i = 0; i < t.rows; ++i)
-      std::memcpy(packed.data() + i * t.L, rows.data() + i * t.stride, sizeof(int32_t) * (size_t)t.L);
+    std::vector<int32_t> packed;
+    if (t.stride == t.L) {
+      packed.swap(rows);
+    } else {
+      packed.resize((size_t)t.rows * t.L);
+      for (int64_t i = 0; i < t.rows; ++i)
+        std::memcpy(packed.data() + i * t.L, rows.data() + i * t.stride, sizeof(int32_t) * (size_t)t.L);
+    }
     dm::Fnv h;
     const int32_t id = t.motif, L = t.L;
     const int64_t R = t.rows;
@@ -151,8 +169,10 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
     dm::Fnv h;
     int32_t id = 0, L = 0;
     int64_t R = 0;
-    if (!dm::rd(F.f, &id, 4, &h) || !dm::rd(F.f, &L, 4, &h) || !dm::rd(F.f, &R, 8, &h) || !dm::motif_def(id) ||
-        !dm::motif_is_table(id) || dm::motif_def(id)->nv != L || R < 0 || R > (int64_t)INT32_MAX) {
+    if (!dm::rd(F.f, &id, 4, &h) || !dm::rd(F.f, &L, 4, &h) || !dm::rd(F.f, &R, 8, &h) ||
+        !(id == DM_MOTIF_APEX ? L == 1 && R >= 0
+                              : (dm::motif_def(id) && dm::motif_is_table(id) && dm::motif_def(id)->nv == L && R >= 0 &&
+                                 R <= (int64_t)INT32_MAX))) {
       drop();
       return dm::fail(DM_ERR_IO, "corrupt motif database file (table header)");
     }
@@ -168,10 +188,16 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
     dm::MotifTable t;
     t.motif = id;
     t.L = L;
-    t.stride = dm::row_stride(L);
+    t.stride = id == DM_MOTIF_APEX ? 1 : dm::row_stride(L);
     t.rows = R;
-    std::vector<int32_t> rows((size_t)R * t.stride, -1);
-    for (int64_t r = 0; r < R; ++r) std::memcpy(rows.data() + r * t.stride, packed.data() + r * L, sizeof(int32_t) * (size_t)L);
+    std::vector<int32_t> rows;
+    if (t.stride == L) {
+      rows.swap(packed);
+    } else {
+      rows.assign((size_t)R * t.stride, -1);
+      for (int64_t r = 0; r < R; ++r)
+        std::memcpy(rows.data() + r * t.stride, packed.data() + r * L, sizeof(int32_t) * (size_t)L);
+    }
     if (cudaMalloc((void **)&t.d_rows, sizeof(int32_t) * std::max<size_t>(rows.size(), 1)) != cudaSuccess ||
         cudaMalloc((void **)&t.d_toff, sizeof(int64_t) * toff.size()) != cudaSuccess ||
         (R > 0 && cudaMemcpy(t.d_rows, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
@@ -185,6 +211,19 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
   }
   std::lock_guard<std::mutex> lk(g->tabs->mu);
   for (auto &t : loaded) {
+    if (t.motif == DM_MOTIF_APEX) {
+      dm::ApexTable &ap = g->tabs->apex;
+      if (ap.entries >= 0) {  // already built: keep the resident one
+        cudaFree(t.d_rows);
+        cudaFree(t.d_toff);
+        continue;
+      }
+      ap.d_apex = t.d_rows;
+      ap.d_toff = t.d_toff;
+      ap.entries = t.rows;
+      ap.build_ms = 0.0;
+      continue;
+    }
     dm::MotifTable &slot = g->tabs->t[dm::motif_bit(t.motif)];
     if (slot.d_toff) {  // already built: keep the resident one
       cudaFree(t.d_rows);

@@ -21,3 +21,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_table" -c 4 -o gpurun_out/prof_c5_full python scripts/prof_step.py c5 1 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pairs_apex" -c 1 -o gpurun_out/prof_c4k4s16_full python scripts/prof_step.py c4-k4-s16 1 > gpurun_out/ncu_k4.log 2>&1
 tail -1 gpurun_out/ncu_full.log gpurun_out/ncu_k4.log
+# multi-rank bench path on one device (gloo collectives; the data path is the library's)
+DM_BENCH_DEVICE=0 DM_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/multi_c5.txt 2>&1
+DM_BENCH_DEVICE=0 DM_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus 2 --steps 2 --warmup 3 --workload c4-diamond-s18 --no-cpu-baseline > gpurun_out/multi_c4d.txt 2>&1
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29535 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > gpurun_out/multi_ref.txt 2>&1
+grep -h '^{' gpurun_out/multi_*.txt | cut -c1-300
+rm -f gpurun_out/sanitize_summary.txt; bash scripts/sanitize.sh > gpurun_out/sanitize.log 2>&1; cat gpurun_out/sanitize_summary.txt

@@ -3,8 +3,9 @@ paper's lattices whose embedding count keeps the CPU oracle within s
 random-walk subgraphs of lattices are trees with 1e7-1e8 labelled embeddings (the oracle needs
 minutes for those), so seeds are screened with a root-sampled oracle estimate and then counted
 exactly; an exact count that does not finish within TIMEOUT seconds drops the seed.  Calls only
-oracle/ and dm_inputs; writes tests/golden/table2_seeds.json.  Usage: pick_table2_seeds.py [lattice ...]
-(default: all; results of other lattices already in the file are kept)."""
+oracle/ and dm_inputs; writes tests/golden/table2_seeds.json.  Usage: pick_table2_seeds.py
+[lattice ...] [--sizes 20,40,...] [--timeout S] (default: all lattices and sizes, 90 s; results of
+other lattices / sizes already in the file are kept)."""
 import json
 import multiprocessing as mp
 import os
@@ -38,13 +39,25 @@ def exact_count(n, e, k, pe):
     return q.get()
 
 
+args = sys.argv[1:]
+sizes = list(LIMIT)
+if "--sizes" in args:
+    i = args.index("--sizes")
+    sizes = [int(x) for x in args[i + 1].split(",")]
+    del args[i:i + 2]
+if "--timeout" in args:
+    i = args.index("--timeout")
+    TIMEOUT = int(args[i + 1])
+    del args[i:i + 2]
 out = json.load(open(PATH))["seeds"] if os.path.exists(PATH) else {}
-todo = sys.argv[1:] or list(LATTICES)
+todo = args or list(LATTICES)
 for name, fn in LATTICES.items():
     if name not in todo:
         continue
     n, e = fn()
     for size, lim in LIMIT.items():
+        if size not in sizes:
+            continue
         picked = []
         seed = 0
         while len(picked) < (5 if size <= 60 else 3) and seed < 120:

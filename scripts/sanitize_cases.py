@@ -1,6 +1,6 @@
 """Small workloads for compute-sanitizer (scripts/sanitize.sh): configs 1-3, R-MAT-10 diamond /
-K4, HH10 P16 count (repeated -> the pipelined sync-free path), a chunked run, the exchange
-kernels.  Counts are checked against the oracle so a silent corruption fails loudly too."""
+K4, HH10 P16 count (repeated -> the pipelined sync-free path), table steps (M7 / heavy-hex motif
+sets), the triangle-apex table and its 4-clique pair step, a chunked run, the exchange kernels.  Counts are checked against the oracle so a silent corruption fails loudly too."""
 import os
 import sys
 
@@ -25,6 +25,20 @@ for (n, e), (k, pe), drop, out in cases:
         if out != "count":
             assert np.array_equal(r.rows, o.rows)
     G.close()
+# table steps (motif database, k_table single / count on 16-bit tiles) and the triangle-apex
+# table with its 4-clique pair step
+n, e = g.ibm_heavy_hex(10)
+G = dm.Graph(n, e)
+want = oracle.match(n, e, *g.path(20), table=False).count
+for rep in range(3):
+    assert G.match(*g.path(20), motifs="M2,M7").count == want
+k, pe, _ = g.random_connected_subgraph(n, e, 16, 1)
+o = oracle.match(n, e, k, pe)
+assert np.array_equal(G.match(k, pe, output="table", motifs="heavy-hex").rows, o.rows)
+nr, er = g.rmat(10, 16, seed=1)
+R = dm.Graph(nr, er, drop_self_loops=True)
+assert R.match(*g.clique(4), motifs="apex").count == oracle.match(nr, er, *g.clique(4), drop_self_loops=True,
+                                                                  table=False).count
 n, e = g.ibm_heavy_hex(6)
 G = dm.Graph(n, e)
 r = G.match(*g.path(10), output="table", mem_budget=1 << 15)

@@ -127,6 +127,19 @@ def test_motif_db_save_load(dm, tmp_path):
     G.save_motifs(path)
     G2 = dm.Graph(n, e[::-1, ::-1].copy())
     G2.load_motifs(path)
+    # the triangle-apex table (a1b) persists too
+    nr, er = g.rmat(11, 16, seed=2)
+    R1 = dm.Graph(nr, er, drop_self_loops=True)
+    R1.build_motifs("apex")
+    rpath = str(tmp_path / "rmat11.dmdb")
+    R1.save_motifs(rpath)
+    R2 = dm.Graph(nr, er, drop_self_loops=True)
+    R2.load_motifs(rpath)
+    assert dm.lib().dm_graph_apex_build_ms(R2._h) == 0.0  # loaded, not built
+    ta, tb = R1.apex_table(), R2.apex_table()
+    assert np.array_equal(ta[0], tb[0]) and np.array_equal(ta[1], tb[1])
+    assert R2.match(*g.clique(4), motifs="apex").count == oracle.match(nr, er, *g.clique(4), drop_self_loops=True,
+                                                                       table=False).count
     for m in ("M5", "M7", "M6-O", "M12-O"):
         a, b = G.motif_table(m), G2.motif_table(m)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and info[m][0] == len(b[0])
