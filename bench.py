@@ -67,8 +67,9 @@ WORKLOADS = {
 # gives the fewest materialized levels and a 6-vertex table tail (measured sets);
 # the other workloads keep the implicit {M2, M3, M3-O}.
 MOTIFS = {"c5": "M2,M7", "c3-p20": "M2,M7",
-          # 4-clique on R-MAT: the triangle-apex table feeds the shared-key pair step
-          "c4-k4": "apex", "c4-k4-s16": "apex"}
+          # diamond / 4-clique on R-MAT: the triangle-apex table feeds the shared-key
+          # pair step (S = apex(u, v) read from the table; every pair still inspected)
+          "c4-k4": "apex", "c4-k4-s16": "apex", "c4-diamond": "apex", "c4-diamond-s18": "apex"}
 
 
 def load_peaks():

@@ -254,14 +254,15 @@ dm_status build_apex_table(const dm_graph *g, cudaStream_t s, ApexTable &t) {
   return DM_OK;
 }
 
-// The apex pair step applies when the step is a shared-key pair step (pair_mode_of >= 0) on
-// rows that are exactly one arc (in_w == 2) and both new vertices key on both columns, with
-// no other filter on the first one (induced non-edges to other columns do not exist at w == 2).
-bool apex_pair_step(const DevStep &st, int elem) {
+// The apex table serves a shared-key pair step (pair_mode_of >= 0) on rows that are exactly one
+// arc (in_w == 2) when both new vertices key on both columns, with no other filter on the first
+// one (induced non-edges to other columns do not exist at w == 2): the closing-edge (4-clique)
+// step runs k_pairs_apex, the others take S from the table in k_pairs.
+bool apex_arc_rows(const DevStep &st, int elem) {
   if (st.in_w != 2 || st.n_new != 2 || elem != 4) return false;
   if (st.n_nbr[0] != 2 || st.n_non[0] != 0) return false;
   const bool keys = (st.nbr[0][0] == 0 && st.nbr[0][1] == 1) || (st.nbr[0][0] == 1 && st.nbr[0][1] == 0);
-  return keys && pair_mode_of(st) == 1;
+  return keys && pair_mode_of(st) >= 0;
 }
 
 cudaError_t launch_pairs_apex(const DevStep &st, const StepIO &io, const dm_graph &g, const ApexTable &t,

@@ -158,11 +158,12 @@ cudaError_t launch_step_single(const DevStep &st, const StepIO &io, const dm_gra
                                int64_t num_tiles, cudaStream_t s);
 int pair_mode_of(const DevStep &st);
 bool row_serial_step(const DevStep &st, const dm_graph &g);
+// apex: optional triangle-apex table; S is then read from it (rows must satisfy apex_arc_rows)
 cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g, int pair_mode,
-                         cudaStream_t s);
+                         cudaStream_t s, const ApexTable *apex = nullptr);
 // shared-key pair step on the triangle-apex table (apex.cu)
 dm_status build_apex_table(const dm_graph *g, cudaStream_t s, ApexTable &t);
-bool apex_pair_step(const DevStep &st, int elem);
+bool apex_arc_rows(const DevStep &st, int elem);  // pair step on arc rows keyed on both columns
 cudaError_t launch_pairs_apex(const DevStep &st, const StepIO &io, const dm_graph &g, const ApexTable &t,
                               cudaStream_t s);
 // deep count-only last step (3..kMaxNew new vertices) on ELL graphs (tail.cu: k_deep)

@@ -186,7 +186,8 @@ cudaError_t launch_count_step(const Ctx &c, int si, const StepIO &io, int64_t ti
   if (is_tab(c, si)) return launch_table(kModeCount, c.tsteps[(size_t)si], io, *c.g, c.tabs[(size_t)si], tiles, c.s);
   const DevStep &D = c.dsteps[(size_t)si];
   const int pm = pair_mode_of(D);
-  if (pm >= 0 && c.apex.d_toff && apex_pair_step(D, io.elem)) return launch_pairs_apex(D, io, *c.g, c.apex, c.s);
+  if (pm >= 0 && c.apex.d_toff && apex_arc_rows(D, io.elem))
+    return pm == 1 ? launch_pairs_apex(D, io, *c.g, c.apex, c.s) : launch_pairs(D, io, *c.g, pm, c.s, &c.apex);
   if (pm >= 0 && !row_serial_step(D, *c.g)) return launch_pairs(D, io, *c.g, pm, c.s);
   return launch_step_count(D, io, *c.g, tiles, c.s);
 }

@@ -15,12 +15,16 @@ namespace {
 // vertex also keys on the first, the closing-edge probe (x0, x1) (pair_mode 1) or the induced
 // non-edge probe (pair_mode 2).  Every candidate pair is inspected (no |S|(|S|-1) shortcut).
 // Persistent grid; warps claim rows in batches; S lives in shared memory (kPairSmem entries)
-// or, for longer anchor lists, in a per-warp global slab of max_degree entries.
+// or, for longer anchor lists, in a per-warp global slab of max_degree entries.  With the
+// triangle-apex table (atoff / aapex) and rows that are exactly one arc whose two
+// columns are both keys, S is read from the table (apex(u, v), u the lower-degree endpoint)
+// instead of being intersected per row; the pairs are inspected the same way.
 template <int NQ>
 __global__ void __launch_bounds__(kStepThreads)
     k_pairs(const DevStep st, const StepIO io_, const int64_t *__restrict__ off,
             const int32_t *__restrict__ adj, int32_t *__restrict__ slab, int64_t slab_cap,
-            int pair_mode, unsigned long long *__restrict__ row_counter) {
+            int pair_mode, unsigned long long *__restrict__ row_counter, const int64_t *__restrict__ atoff,
+            const int32_t *__restrict__ aapex) {
   StepIO io = io_;  // device-written input size (sync-free chaining)
   if (!resolve_in_rows(io)) return;
   constexpr int kWarps = kStepThreads / 32;
@@ -44,28 +48,45 @@ __global__ void __launch_bounds__(kStepThreads)
       for (int c = lane; c < ws; c += 32)
         row[c] = io.in ? __ldg(io.in + r * ws + c) : (c == 0 ? (int32_t)(io.seed_base + r) : -1);
       __syncwarp();
-      int32_t av;
-      int64_t ad;
-      const int ac = pick_anchor(st, 0, row, w, 0, off, av, ad);
-      const int64_t e0 = __ldg(off + av);
-      int32_t *S = ad <= kPairSmem ? s_list[wl] : gslab;
-      // ---- S: accepted first-vertex candidates, in anchor-list (ascending) order
+      int32_t *S;
       int ns = 0;
-      uint32_t pr = 0;
-      for (int64_t i0 = 0; i0 < ad; i0 += 32) {
-        const int64_t i = i0 + lane;
-        bool ok = false;
-        int32_t x = -1;
-        if (i < ad) {
-          x = __ldg(adj + e0 + i);
-          ok = accept<NQ>(st, 0, row, w, ws, 0, x, ac, off, adj, pr);
+      if (aapex) {  // S = apex(u, v): one lookup instead of a per-row intersection
+        const int64_t d0 = degree(off, row[0]), d1 = degree(off, row[1]);
+        const int32_t u = d0 <= d1 ? row[0] : row[1], v = d0 <= d1 ? row[1] : row[0];
+        int64_t lo = __ldg(off + u), hi = __ldg(off + u + 1);
+        while (lo < hi) {
+          const int64_t m = (lo + hi) >> 1;
+          if (__ldg(adj + m) < v) lo = m + 1;
+          else hi = m;
         }
-        const unsigned m = __ballot_sync(0xffffffffu, ok);
-        if (ok) S[ns + __popc(m & lt)] = x;
-        ns += __popc(m);
+        const int64_t s0 = __ldg(atoff + lo);
+        ns = (int)(__ldg(atoff + lo + 1) - s0);
+        S = ns <= kPairSmem ? s_list[wl] : gslab;
+        for (int i = lane; i < ns; i += 32) S[i] = __ldg(adj + __ldg(aapex + s0 + i));
+        cand += (lane == 0) ? (unsigned long long)ns : 0ull;
+      } else {
+        int32_t av;
+        int64_t ad;
+        const int ac = pick_anchor(st, 0, row, w, 0, off, av, ad);
+        const int64_t e0 = __ldg(off + av);
+        S = ad <= kPairSmem ? s_list[wl] : gslab;
+        // ---- S: accepted first-vertex candidates, in anchor-list (ascending) order
+        uint32_t pr = 0;
+        for (int64_t i0 = 0; i0 < ad; i0 += 32) {
+          const int64_t i = i0 + lane;
+          bool ok = false;
+          int32_t x = -1;
+          if (i < ad) {
+            x = __ldg(adj + e0 + i);
+            ok = accept<NQ>(st, 0, row, w, ws, 0, x, ac, off, adj, pr);
+          }
+          const unsigned m = __ballot_sync(0xffffffffu, ok);
+          if (ok) S[ns + __popc(m & lt)] = x;
+          ns += __popc(m);
+        }
+        probes += pr;
+        cand += (lane == 0) ? (unsigned long long)ad : 0ull;
       }
-      probes += pr;
-      cand += (lane == 0) ? (unsigned long long)ad : 0ull;
       __syncwarp();
       // ---- every ordered pair of S
       const int64_t np = (int64_t)ns * ns;
@@ -213,7 +234,7 @@ int pair_mode_of(const DevStep &st) {
 }
 
 cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g, int pair_mode,
-                         cudaStream_t s) {
+                         cudaStream_t s, const ApexTable *apex) {
   if (io.in_rows <= 0 && !io.d_in_rows) return cudaSuccess;
   auto kern = k_pairs<0>;
   switch (row_stride(st.in_w) >> 2) {
@@ -242,7 +263,8 @@ cudaError_t launch_pairs(const DevStep &st, const StepIO &io, const dm_graph &g,
     return e;
   }
   cudaMemsetAsync(counter, 0, sizeof(unsigned long long), s);
-  kern<<<(unsigned)grid, kStepThreads, 0, s>>>(st, io, g.d_off, g.d_adj, slab, cap, pair_mode, counter);
+  kern<<<(unsigned)grid, kStepThreads, 0, s>>>(st, io, g.d_off, g.d_adj, slab, cap, pair_mode, counter,
+                                                apex ? apex->d_toff : nullptr, apex ? apex->d_apex : nullptr);
   e = cudaGetLastError();
   cudaFreeAsync(slab, s);
   cudaFreeAsync(counter, s);
