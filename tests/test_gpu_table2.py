@@ -51,8 +51,12 @@ def test_table2_tables(dm, lattice, size):
         assert r.count == o.count and np.array_equal(r.rows, o.rows)
 
 
-@pytest.mark.parametrize("size", [80, 100])
-@pytest.mark.parametrize("lattice", list(LATTICES))
+# grid60/100: no seed among those tried had an oracle count finishing within the picker's time
+# limit (the oracle's depth-first order explodes on those patterns), so that cell has no case
+LARGE = [(lat, size) for lat in LATTICES for size in (80, 100) if f"{lat}/{size}" in SEEDS]
+
+
+@pytest.mark.parametrize("lattice,size", LARGE)
 def test_table2_counts_large_patterns(dm, lattice, size):
     """80- and 100-vertex patterns (beyond the round-1 cap of 64): counts against the oracle's
     counts stored by scripts/pick_table2_seeds.py (the oracle needs up to ~70 s per lattice here)."""
