@@ -98,7 +98,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -132,7 +132,7 @@ class ClockSampler:
                 if v.lower() == "active":
                     reasons.add(nm)
         note = None
-        if not sms:  # timed region shorter than the 100 ms sampling period: one sample right after it
+        if not sms:  # timed region shorter than the 20 ms sampling period: one sample right after it
             try:
                 ln = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
@@ -143,7 +143,7 @@ class ClockSampler:
                 for nm, v in zip(names, parts[3:7]):
                     if v.lower() == "active":
                         reasons.add(nm)
-                note = "timed region < 100 ms: one sample taken right after it"
+                note = "timed region < 20 ms: one sample taken right after it"
             except Exception:
                 pass
         out = {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,

@@ -97,8 +97,8 @@ __global__ void __launch_bounds__(kApexThreads)
 // the probe -- a re-association of the pair step, every candidate of that join is
 // inspected, and injectivity holds by construction (x1 is in N(u) ∩ N(x0) ∩ N(v), no self-loops).
 // Only the closing-edge pair step (4-clique) uses it: the distinct-pairs (diamond) and induced
-// non-edge pair steps keep pairs.cu, which inspects every pair of S (no count-mode
-// shortcut that skips inspecting candidates).
+// non-edge pair steps keep pairs.cu (with S read from this table), which inspects every pair of
+// S (no count-mode shortcut that skips inspecting candidates).
 __global__ void __launch_bounds__(kStepThreads)
     k_pairs_apex(const StepIO io_, const int64_t *__restrict__ off, const int32_t *__restrict__ adj,
                  const int64_t *__restrict__ toff, const int32_t *__restrict__ apex,

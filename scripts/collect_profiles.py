@@ -33,14 +33,16 @@ for f in sorted(glob.glob("gpurun_out/*.ncu-rep")):
     r = subprocess.run(["ncu", "-i", f, "--page", "raw", "--csv"], capture_output=True, text=True)
     rows = list(csv.reader(r.stdout.splitlines()))
     if len(rows) > 2:
-        h = rows[0]
+        h, units = rows[0], dict(zip(rows[0], rows[1]))  # second row: the unit of every column
         for row in rows[2:]:
             d = dict(zip(h, row))
             try:
-                rd = float(d["dram__bytes_read.sum"]) ; wr = float(d["dram__bytes_write.sum"])
+                rd = float(d["dram__bytes_read.sum"].replace(",", ""))
+                wr = float(d["dram__bytes_write.sum"].replace(",", ""))
             except Exception:
                 continue
-            out.append(f"{d['ID']:>2} {d['Kernel Name'][:48]:48s} dram read {rd:.4g} B, write {wr:.4g} B")
+            ur, uw = units.get("dram__bytes_read.sum", "?"), units.get("dram__bytes_write.sum", "?")
+            out.append(f"{d['ID']:>2} {d['Kernel Name'][:48]:48s} dram read {rd:.4g} {ur}, write {wr:.4g} {uw}")
     out += ["```", ""]
 for f in sorted(glob.glob("gpurun_out/steps_*.txt")):
     out += [f"## per-step statistics ({os.path.basename(f)})", "```", open(f).read().strip(), "```", ""]

@@ -26,4 +26,3 @@ DM_BENCH_DEVICE=0 DM_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.r
 DM_BENCH_DEVICE=0 DM_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus 2 --steps 2 --warmup 3 --workload c4-diamond-s18 --no-cpu-baseline > gpurun_out/multi_c4d.txt 2>&1
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29535 bench.py --impl reference --gpus 2 --steps 1 --warmup 1 > gpurun_out/multi_ref.txt 2>&1
 grep -h '^{' gpurun_out/multi_*.txt | cut -c1-300
-rm -f gpurun_out/sanitize_summary.txt; bash scripts/sanitize.sh > gpurun_out/sanitize.log 2>&1; cat gpurun_out/sanitize_summary.txt
