@@ -19,7 +19,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdeltamotif.so")
+# DM_LIBRARY_VARIANT=checked loads the bounds-checked build (device asserts trap on a bad index)
+LIB_PATH = os.path.join(_HERE, "libdeltamotif_checked.so" if os.environ.get("DM_LIBRARY_VARIANT") == "checked"
+                        else "libdeltamotif.so")
 
 DM_OK = 0
 ERRORS = {-1: "DM_ERR_ARG", -2: "DM_ERR_VERTEX_RANGE", -3: "DM_ERR_SELF_LOOP",

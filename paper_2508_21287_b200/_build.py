@@ -9,6 +9,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libdeltamotif.so")
+# checked variant: device bounds checks (DM_DCHECK, -DDM_CHECKED) trap on a bad index; loaded
+# when DM_LIBRARY_VARIANT=checked (tests/test_gpu_checked.py)
+LIB_CHECKED = os.path.join(PKG, "libdeltamotif_checked.so")
 SOURCES = ["errors.cpp", "planner.cpp", "graph.cu", "extend.cu", "tail.cu", "pairs.cu", "apex.cu", "exchange.cu", "tabstep.cu", "motifdb.cu", "scoring.cu", "match.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -16,23 +19,26 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "deltamotif.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    objdir = os.path.join(PKG, "build")
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """libdeltamotif.so, or with checked=True libdeltamotif_checked.so (-DDM_CHECKED)."""
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib):
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    objdir = os.path.join(PKG, "build_checked" if checked else "build")
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
     headers.append(os.path.join(ROOT, "include", "deltamotif.h"))
     newest_hdr = max(os.path.getmtime(h) for h in headers)
+    flags = FLAGS + (["-DDM_CHECKED"] if checked else [])
     objs, procs = [], []
     for src in SOURCES:  # one nvcc per translation unit, in parallel; stale objects only
         obj = os.path.join(objdir, src + ".o")
@@ -41,7 +47,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if (not force and os.path.exists(obj)
                 and os.path.getmtime(obj) > max(os.path.getmtime(spath), newest_hdr)):
             continue
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", spath, "-o", obj + ".tmp"]
+        cmd = [NVCC, *ARCH, *flags, "-c", spath, "-o", obj + ".tmp"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd), obj))
@@ -50,9 +56,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise subprocess.CalledProcessError(p.returncode, "nvcc")
         os.replace(obj + ".tmp", obj)
     subprocess.check_call([NVCC, *ARCH, "-shared", *objs, "-o", tmp])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

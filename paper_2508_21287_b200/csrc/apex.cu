@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kApexThreads)
       }
       const unsigned m = __ballot_sync(0xffffffffu, hit);
       if (WRITE) {
+        DM_DCHECK(!hit || pos + __popc(m & lt) < cnt_toff[e + 1]);
         if (hit) apex[pos + __popc(m & lt)] = (int32_t)arc;
         pos += __popc(m);
       } else {
@@ -127,11 +128,14 @@ __global__ void __launch_bounds__(kStepThreads)
       const int32_t u = da <= db ? ab.x : ab.y, v = da <= db ? ab.y : ab.x;
       const int64_t lu = __ldg(off + u), hu = __ldg(off + u + 1);
       const int64_t e = lower_bound_g(adj, lu, hu, v);  // arc (u, v): every lane, broadcast loads
+      DM_DCHECK(e < hu && __ldg(adj + e) == v);        // the rows are arcs
       const int64_t s0 = __ldg(toff + e), ns = __ldg(toff + e + 1) - s0;
+      DM_DCHECK(ns >= 0 && ns <= hu - lu);
       if (lane == 0) cand += (unsigned long long)ns;
       if (ns < 2) continue;
       for (int64_t i = lane; i < ns; i += 32) {
         const int64_t p = __ldg(apex + s0 + i) - lu;
+        DM_DCHECK(p >= 0 && p < hu - lu && (p >> 5) < bm_words);  // positions in N(u)
         atomicOr(B + (p >> 5), 1u << (p & 31));
       }
       __syncwarp();
@@ -170,6 +174,7 @@ __global__ void __launch_bounds__(kStepThreads)
           const bool va = ja < total, vb = jb < total;
           const int64_t qa = (va ? __ldg(apex + tka + (ja - eka)) : lu) - lu;
           const int64_t qb = (vb ? __ldg(apex + tkb + (jb - ekb)) : lu) - lu;
+          DM_DCHECK(qa >= 0 && qa < hu - lu && qb >= 0 && qb < hu - lu);  // apex(u, x0) ⊆ N(u)
           edges += va & ((B[qa >> 5] >> (qa & 31)) & 1u);
           edges += vb & ((B[qb >> 5] >> (qb & 31)) & 1u);
         }

@@ -78,6 +78,19 @@ struct DeviceGuard {
   }
 };
 
+// Device-side bounds checks of the checked build (libdeltamotif_checked.so, -DDM_CHECKED): a
+// failed check traps the kernel (the launch then reports an error); compiled out otherwise.
+#ifdef DM_CHECKED
+#define DM_DCHECK(cond) \
+  do {              \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define DM_DCHECK(cond) \
+  do {              \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------- join-step kernel interface
 constexpr int kStepThreads = 256;   // threads per CTA
 constexpr int kTileRows = 256;      // frontier rows per CTA tile
@@ -185,6 +198,7 @@ struct DevTabStep {
   int32_t in_w, n_new;
   int32_t key0, key1, skip;  // row columns bound to template positions 0 / 1; known-duplicate column
   int32_t L, tstride;        // template vertices, table row stride (words)
+  int64_t trows;             // |Res(M)| (bounds of the checked build)
   int32_t n_eq, n_pr;
   uint32_t newmask;          // bit p: template position p is a new vertex
   uint32_t eqmask;           // bit p: template position p must equal row[eq_colp[p]]

@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(kStepThreads)
         const int64_t s0 = __ldg(atoff + lo);
         ns = (int)(__ldg(atoff + lo + 1) - s0);
         S = ns <= kPairSmem ? s_list[wl] : gslab;
+        DM_DCHECK(lo < __ldg(off + u + 1) && __ldg(adj + lo) == v && (ns <= kPairSmem || ns <= slab_cap));
         for (int i = lane; i < ns; i += 32) S[i] = __ldg(adj + __ldg(aapex + s0 + i));
         cand += (lane == 0) ? (unsigned long long)ns : 0ull;
       } else {

@@ -245,6 +245,7 @@ __global__ void __launch_bounds__(kStepThreads)
     const int loc = (int)(j - exr);
     const int4 meta = s_meta[r];
     const int ei = loc < meta.y ? meta.x + loc : meta.z + (loc - meta.y);
+    DM_DCHECK(r < nrows && ei >= 0 && ei < st.trows);
     ++my_cand;
     const int4 *ent = reinterpret_cast<const int4 *>(tab + (int64_t)ei * TS);
 #pragma unroll
@@ -476,6 +477,7 @@ DevTabStep make_dev_tab_step(const Step &s, const MotifTable &t) {
   d.skip = s.skip;
   d.L = t.L;
   d.tstride = t.stride;
+  d.trows = t.rows;
   d.n_eq = s.n_eq;
   for (int i = 0; i < s.n_eq; ++i) {
     d.eq_pos[i] = (int8_t)s.eq_pos[i];
