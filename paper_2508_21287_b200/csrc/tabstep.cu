@@ -77,8 +77,11 @@ __device__ __forceinline__ uint32_t filt_hash(int32_t v) { return ((uint32_t)v *
 
 // 16-bit levels (R16): the tile is kept in shared memory as the stored uint16 ids (half the bytes
 // of widened rows: more CTAs per SM), rows padded to an odd number of 16-byte chunks
-// (conflict-free LDS.128 across lanes); the exact all-distinct scan compares two ids per 32-bit
-// word (__vcmpeq2; padding 0xFFFF is never an id since n <= 65535).
+// (conflict-free LDS.128 across lanes); the exact all-distinct scan tests two ids per 32-bit
+// word: t = word ^ (x | x << 16) has a zero half iff x is one of them, detected branch-free by
+// (t - 0x00010001) & ~t & 0x80008000 (a borrow from a zero low half can only add a report when a
+// zero half exists already); padding 0xFFFF is never an id since n <= 65535.  __vcmpeq2 is
+// emulated on sm_100 (~6 instructions per word).
 __host__ __device__ inline int smem_stride16(int w) {
   const int rs = row_stride16(w);
   return ((rs >> 3) & 1) ? rs : rs + 8;
@@ -87,9 +90,10 @@ __device__ __forceinline__ bool in_row16(const uint16_t *row, int nq8, int32_t x
   const uint32_t xx = (uint32_t)x * 0x10001u;
   const uint4 *r4 = reinterpret_cast<const uint4 *>(row);
   uint32_t hit = 0;
+  auto zero_half = [](uint32_t t) { return (t - 0x00010001u) & ~t & 0x80008000u; };
   for (int q = 0; q < nq8; ++q) {
     const uint4 v = r4[q];
-    hit |= __vcmpeq2(v.x, xx) | __vcmpeq2(v.y, xx) | __vcmpeq2(v.z, xx) | __vcmpeq2(v.w, xx);
+    hit |= zero_half(v.x ^ xx) | zero_half(v.y ^ xx) | zero_half(v.z ^ xx) | zero_half(v.w ^ xx);
   }
   return hit != 0u;
 }
