@@ -358,7 +358,11 @@ __global__ void __launch_bounds__(kStepThreads)
             continue;
           }
           int32_t v[8];
-          if constexpr (R16) {
+          if (!all_parent && tail_fast) {
+            // every column of this chunk is in the staged tail (nothing from the parent row)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = -1;
+          } else if constexpr (R16) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[i] = (i < per && c0 + i < w) ? RV(pr, c0 + i) : -1;
           } else {
