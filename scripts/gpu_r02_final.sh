@@ -18,6 +18,7 @@ python scripts/prof_step.py c5 3 > gpurun_out/steps_c5.txt 2>&1
 python scripts/prof_step.py c4-k4-s16 2 > gpurun_out/steps_c4k4s16.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c5.csv python scripts/prof_step.py c5 1 > gpurun_out/prof_c5.txt 2>&1
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c4-k4.csv python scripts/prof_step.py c4-k4 1 > gpurun_out/prof_c4k4.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c4-diamond.csv python scripts/prof_step.py c4-diamond 1 > gpurun_out/prof_c4d.txt 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_table" -c 4 -o gpurun_out/prof_c5_full python scripts/prof_step.py c5 1 > gpurun_out/ncu_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_pairs_apex" -c 1 -o gpurun_out/prof_c4k4s16_full python scripts/prof_step.py c4-k4-s16 1 > gpurun_out/ncu_k4.log 2>&1
 tail -1 gpurun_out/ncu_full.log gpurun_out/ncu_k4.log

@@ -35,6 +35,18 @@ def test_exports_every_header_symbol(dm):
         assert getattr(raw, s) is not None
 
 
+def test_checked_variant_exports_every_header_symbol():
+    """The bounds-checked build (DM_LIBRARY_VARIANT=checked) is the same ABI with device asserts."""
+    import subprocess
+    import sys
+    code = ("import ctypes, paper_2508_21287_b200 as dm; assert dm.LIB_PATH.endswith('libdeltamotif_checked.so'); "
+            "L = dm.lib(); assert L.dm_abi_version() == dm.ABI_VERSION; "
+            "raw = ctypes.CDLL(dm.LIB_PATH); [getattr(raw, s) for s in dm.EXPORTS]; print('ok')")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=300,
+                       env=dict(os.environ, DM_LIBRARY_VARIANT="checked"))
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stderr[-2000:]
+
+
 def test_abi_version_and_opts_defaults(dm):
     L = dm.lib()
     assert L.dm_abi_version() == dm.ABI_VERSION
