@@ -204,6 +204,7 @@ __global__ void __launch_bounds__(kStepThreads)
 }  // namespace
 
 dm_status build_apex_table(const dm_graph *g, cudaStream_t s, ApexTable &t) {
+  NvtxRange nvtx("triangle-apex table");
   const int64_t arcs = g->arcs;
   if (arcs >= (int64_t)INT32_MAX) return fail(DM_ERR_UNSUPPORTED, "apex table needs < 2^31 arcs");
   const auto t_start = std::chrono::steady_clock::now();

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <cstdint>
 #include <mutex>
@@ -90,6 +91,14 @@ struct DeviceGuard {
   do {              \
   } while (0)
 #endif
+
+// NVTX range for profilers (header-only NVTX v3: free when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange &) = delete;
+  NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // ------------------------------------------------------------- join-step kernel interface
 constexpr int kStepThreads = 256;   // threads per CTA

@@ -276,6 +276,7 @@ extern "C" {
 dm_status dm_graph_create(int32_t n, const int32_t *edges, int64_t m, int32_t flags,
                           int32_t device, dm_graph **out) {
   dm::clear_error();
+  dm::NvtxRange nvtx("dm_graph_create");
   return dm::graph_create_impl(n, edges, m, flags, device, out);
 }
 

@@ -267,6 +267,9 @@ dm_status write_tiles(Ctx &c, int si, const StepIO &base_io, const uint64_t *d_e
 
 dm_status run_step(Ctx &c, int si, const int32_t *in, int64_t in_rows, int64_t seed_base) {
   if (in_rows <= 0) return DM_OK;
+  char nvtx_name[32];
+  std::snprintf(nvtx_name, sizeof(nvtx_name), "join step %d", si);
+  NvtxRange nvtx(nvtx_name);
   if (si == c.stop_at) {  // dm_match_prefix: append this (chunk of the) level to the collector
     const int Win = row_stride(c.dsteps[(size_t)si].in_w);
     if (c.front_rows + (uint64_t)in_rows > c.front_cap) {
@@ -477,6 +480,7 @@ bool async_eligible(const Ctx &c) {
 // done = true when the match completed on this path (count in c.d_acc, stats filled)
 dm_status run_async(Ctx &c, const std::vector<double> &ratio, int64_t seed_rows, int64_t seed_base,
                     bool &done) {
+  NvtxRange nvtx("join steps (sync-free chain)");
   done = false;
   const int nsteps = (int)c.plan->steps.size();
   std::vector<uint64_t> cap((size_t)nsteps, 0);
@@ -782,6 +786,7 @@ dm_status check_plan(const Plan &plan, const dm_graph *g, bool table) {
 dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64_t pm,
                      const dm_match_opts *opt_in, dm_result **out, const RunSpec &rs = RunSpec()) {
   if (!g || (!out && !rs.fout)) return fail(DM_ERR_ARG, "graph/out is NULL");
+  NvtxRange nvtx("dm_match");
   static const bool trace = std::getenv("DM_TRACE_HOST") != nullptr;  // debug: host phase times
   auto t_start = std::chrono::steady_clock::now();
   auto tr = [&](const char *what) {
@@ -1048,6 +1053,7 @@ dm_status match_impl(const dm_graph *g, int32_t k, const int32_t *p_edges, int64
 }
 
 dm_status build_motif_table(const dm_graph *g, int id, cudaStream_t s, uint64_t row_budget, MotifTable &t) {
+  NvtxRange nvtx("motif table (Alg. 2)");
   const MotifDef *M = motif_def(id);
   if (!M || !motif_is_table(id)) return fail(DM_ERR_ARG, "not a table motif");
   const auto t0 = std::chrono::steady_clock::now();

@@ -102,6 +102,7 @@ dm_status dm_score_layouts(const dm_graph *g, int32_t k, const int32_t *p_edges,
                            int64_t fm, const dm_match_opts *opt, int64_t top_k, int32_t *rows_out,
                            double *scores_out, int64_t *n_out, uint64_t *count_out) {
   dm::clear_error();
+  dm::NvtxRange nvtx("dm_score_layouts");
   if (!g || !node_fid || (fm > 0 && (!fid_edges || !fid_vals)) || fm < 0 || !n_out)
     return dm::fail(DM_ERR_ARG, "NULL argument");
   if (top_k <= 0) return dm::fail(DM_ERR_ARG, "top_k must be positive");
