@@ -149,7 +149,11 @@ DM_API int32_t dm_abi_version(void);
  *   out    receives the handle (free with dm_graph_destroy)
  * Errors: DM_ERR_ARG, DM_ERR_VERTEX_RANGE, DM_ERR_SELF_LOOP, DM_ERR_OOM, DM_ERR_CUDA.
  * The build runs on device (sort, dedup, degree scan) and is the "data preparation" phase
- * the paper times separately.
+ * the paper times separately.  All device buffers of a graph (CSR, motif tables,
+ * apex table) come from the device's stream-ordered memory pool, whose release threshold the
+ * library raises so create / destroy cycles reuse memory.  dm_graph_destroy must not be called
+ * while work on g is in flight (every dm_* call returns after its stream work completed); it
+ * returns the buffers to the pool without a device-wide synchronisation.
  */
 DM_API dm_status dm_graph_create(int32_t n, const int32_t *edges, int64_t m, int32_t flags,
                           int32_t device, dm_graph **out);

@@ -92,6 +92,11 @@ struct DeviceGuard {
   } while (0)
 #endif
 
+// The device's default stream-ordered memory pool keeps freed memory (release threshold = max):
+// frontier levels, motif tables and the graph itself are allocated from it, so repeated queries and
+// graph create / destroy cycles do not return memory to the driver (graph.cu).
+void configure_pool(int device);
+
 // NVTX range for profilers (header-only NVTX v3: free when no tool is attached)
 struct NvtxRange {
   explicit NvtxRange(const char *name) { nvtxRangePushA(name); }

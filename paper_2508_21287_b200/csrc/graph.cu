@@ -123,6 +123,19 @@ int grid_for(int64_t work) {
 
 }  // namespace
 
+void configure_pool(int device) {
+  static std::mutex mu;
+  static bool done[64] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done[device] = true;
+}
+
 static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, int32_t flags,
                                    int32_t device, dm_graph **out) {
   if (!out) return fail(DM_ERR_ARG, "out is NULL");
@@ -134,6 +147,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   if (device < 0 || device >= ndev) return fail(DM_ERR_ARG, "bad device ordinal");
   DeviceGuard dg(device);
   if (!dg.ok) return fail(DM_ERR_CUDA, "cudaSetDevice failed");
+  configure_pool(device);
   cudaStream_t s;
   DM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
   struct StreamGuard {
@@ -158,20 +172,25 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   int64_t *d_nsel = nullptr;
   int *d_err = nullptr;
   void *d_tmp = nullptr;
+  // every device buffer comes from the stream-ordered pool (create / destroy cycles reuse memory)
+  auto release = [&](void *p) {
+    if (p) cudaFreeAsync(p, s);
+  };
   auto cleanup = [&]() {
-    cudaFree(d_edges);
-    cudaFree(d_keys);
-    cudaFree(d_sorted);
-    cudaFree(d_uniq);
-    cudaFree(d_nsel);
-    cudaFree(d_err);
-    cudaFree(d_tmp);
+    release(d_edges);
+    release(d_keys);
+    release(d_sorted);
+    release(d_uniq);
+    release(d_nsel);
+    release(d_err);
+    release(d_tmp);
   };
   auto bail = [&](dm_status st) {
     cleanup();
-    cudaFree(g->d_off);
-    cudaFree(g->d_adj);
-    cudaFree(g->d_ell);
+    release(g->d_off);
+    release(g->d_adj);
+    release(g->d_ell);
+    cudaStreamSynchronize(s);
     delete g->tabs;
     delete g;
     return st;
@@ -184,16 +203,16 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
                        std::string(#call " failed: ") + cudaGetErrorString(_e)));          \
   } while (0)
 
-  GC(cudaMalloc(&g->d_off, sizeof(int64_t) * ((size_t)n + 1)));
-  GC(cudaMalloc(&d_err, sizeof(int)));
+  GC(cudaMallocAsync(&g->d_off, sizeof(int64_t) * ((size_t)n + 1), s));
+  GC(cudaMallocAsync(&d_err, sizeof(int), s));
   GC(cudaMemsetAsync(d_err, 0, sizeof(int), s));
   int64_t arcs = 0;
   if (m > 0) {
-    GC(cudaMalloc(&d_edges, sizeof(int32_t) * 2 * (size_t)m));
-    GC(cudaMalloc(&d_keys, sizeof(unsigned long long) * (size_t)nk));
-    GC(cudaMalloc(&d_sorted, sizeof(unsigned long long) * (size_t)nk));
-    GC(cudaMalloc(&d_uniq, sizeof(unsigned long long) * (size_t)nk));
-    GC(cudaMalloc(&d_nsel, sizeof(int64_t)));
+    GC(cudaMallocAsync(&d_edges, sizeof(int32_t) * 2 * (size_t)m, s));
+    GC(cudaMallocAsync(&d_keys, sizeof(unsigned long long) * (size_t)nk, s));
+    GC(cudaMallocAsync(&d_sorted, sizeof(unsigned long long) * (size_t)nk, s));
+    GC(cudaMallocAsync(&d_uniq, sizeof(unsigned long long) * (size_t)nk, s));
+    GC(cudaMallocAsync(&d_nsel, sizeof(int64_t), s));
     GC(cudaMemcpyAsync(d_edges, edges, sizeof(int32_t) * 2 * (size_t)m, cudaMemcpyHostToDevice, s));
     k_make_arcs<<<grid_for(m), 256, 0, s>>>(d_edges, m, n, flags & DM_GRAPH_DROP_SELF_LOOPS,
                                             d_keys, d_err);
@@ -209,7 +228,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
     GC(cub::DeviceRadixSort::SortKeys(nullptr, tmp_sort, d_keys, d_sorted, nk, 0, end_bit, s));
     GC(cub::DeviceSelect::Unique(nullptr, tmp_uniq, d_sorted, d_uniq, d_nsel, nk, s));
     size_t tmp = std::max(tmp_sort, tmp_uniq);
-    GC(cudaMalloc(&d_tmp, tmp));
+    GC(cudaMallocAsync(&d_tmp, tmp, s));
     GC(cub::DeviceRadixSort::SortKeys(d_tmp, tmp, d_keys, d_sorted, nk, 0, end_bit, s));
     GC(cub::DeviceSelect::Unique(d_tmp, tmp, d_sorted, d_uniq, d_nsel, nk, s));
     int64_t nsel = 0;
@@ -223,7 +242,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
     }
   }
   g->arcs = arcs;
-  GC(cudaMalloc(&g->d_adj, sizeof(int32_t) * (size_t)std::max<int64_t>(arcs, 1)));
+  GC(cudaMallocAsync(&g->d_adj, sizeof(int32_t) * (size_t)std::max<int64_t>(arcs, 1), s));
   if (arcs > 0) {
     k_bounds<<<grid_for(arcs + 1), 256, 0, s>>>(d_uniq, arcs, n, g->d_off, g->d_adj);
     GC(cudaGetLastError());
@@ -241,7 +260,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
   g->max_deg = hmax;
   if (n > 0 && arcs > 0) {  // statistics for the join-order cost model
     double *d_stat = nullptr;
-    GC(cudaMalloc(&d_stat, 3 * sizeof(double)));
+    GC(cudaMallocAsync(&d_stat, 3 * sizeof(double), s));
     GC(cudaMemsetAsync(d_stat, 0, 3 * sizeof(double), s));
     k_sum_d2<<<grid_for(n), 256, 0, s>>>(g->d_off, n, d_stat);
     const int samples = 4096;
@@ -250,7 +269,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
     cudaError_t e1 = cudaGetLastError();
     cudaError_t e2 = cudaMemcpyAsync(hs, d_stat, sizeof(hs), cudaMemcpyDeviceToHost, s);
     cudaError_t e3 = cudaStreamSynchronize(s);
-    cudaFree(d_stat);
+    cudaFreeAsync(d_stat, s);
     GC(e1);
     GC(e2);
     GC(e3);
@@ -258,7 +277,7 @@ static dm_status graph_create_impl(int32_t n, const int32_t *edges, int64_t m, i
     g->closure = hs[2] > 0 ? hs[1] / hs[2] : 0.0;
   }
   if (n > 0 && hmax <= 4) {
-    GC(cudaMalloc(&g->d_ell, sizeof(int4) * (size_t)n));
+    GC(cudaMallocAsync(&g->d_ell, sizeof(int4) * (size_t)n, s));
     k_build_ell<<<grid_for(n), 256, 0, s>>>(g->d_off, g->d_adj, n, reinterpret_cast<int4 *>(g->d_ell));
     GC(cudaGetLastError());
     GC(cudaStreamSynchronize(s));
@@ -280,21 +299,27 @@ dm_status dm_graph_create(int32_t n, const int32_t *edges, int64_t m, int32_t fl
   return dm::graph_create_impl(n, edges, m, flags, device, out);
 }
 
+// Every buffer of a graph comes from the device's stream-ordered pool; no work on g is in flight
+// when it is destroyed (dm_match and the step-level calls return after their stream work), so
+// the buffers go back to the pool in legacy-stream order without a device-wide synchronisation.
 void dm_graph_destroy(dm_graph *g) {
   if (!g) return;
   dm::DeviceGuard dg(g->device);
+  auto release = [](void *p) {
+    if (p) cudaFreeAsync(p, nullptr);
+  };
   if (g->tabs) {
     for (auto &t : g->tabs->t) {
-      cudaFree(t.d_rows);
-      cudaFree(t.d_toff);
+      release(t.d_rows);
+      release(t.d_toff);
     }
-    cudaFree(g->tabs->apex.d_toff);
-    cudaFree(g->tabs->apex.d_apex);
+    release(g->tabs->apex.d_toff);
+    release(g->tabs->apex.d_apex);
     delete g->tabs;
   }
-  cudaFree(g->d_off);
-  cudaFree(g->d_adj);
-  cudaFree(g->d_ell);
+  release(g->d_off);
+  release(g->d_adj);
+  release(g->d_ell);
   delete g;
 }
 

@@ -656,17 +656,6 @@ cudaError_t cached_mem_info(int device, size_t *fr, size_t *tot) {
   return e;
 }
 
-void configure_pool(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done[device] = true;
-}
-
 // Per-row work estimate of the next step (for frontier rebalancing): degree of the first new
 // vertex's anchor key raised to the number of new vertices.
 __global__ void k_row_work(const int32_t *__restrict__ rows, int64_t n, int stride, const DevStep st,

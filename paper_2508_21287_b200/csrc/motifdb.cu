@@ -160,8 +160,8 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
   std::vector<dm::MotifTable> loaded;
   auto drop = [&]() {
     for (auto &t : loaded) {
-      cudaFree(t.d_rows);
-      cudaFree(t.d_toff);
+      if (t.d_rows) cudaFreeAsync(t.d_rows, nullptr);
+      if (t.d_toff) cudaFreeAsync(t.d_toff, nullptr);
     }
   };
   dm::DeviceGuard dg(g->device);
@@ -198,12 +198,14 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
       for (int64_t r = 0; r < R; ++r)
         std::memcpy(rows.data() + r * t.stride, packed.data() + r * L, sizeof(int32_t) * (size_t)L);
     }
-    if (cudaMalloc((void **)&t.d_rows, sizeof(int32_t) * std::max<size_t>(rows.size(), 1)) != cudaSuccess ||
-        cudaMalloc((void **)&t.d_toff, sizeof(int64_t) * toff.size()) != cudaSuccess ||
+    // graph-owned buffers come from the stream-ordered pool (legacy stream: ordered before the
+    // synchronous copies below; released by dm_graph_destroy)
+    if (cudaMallocAsync((void **)&t.d_rows, sizeof(int32_t) * std::max<size_t>(rows.size(), 1), nullptr) != cudaSuccess ||
+        cudaMallocAsync((void **)&t.d_toff, sizeof(int64_t) * toff.size(), nullptr) != cudaSuccess ||
         (R > 0 && cudaMemcpy(t.d_rows, rows.data(), sizeof(int32_t) * rows.size(), cudaMemcpyHostToDevice) != cudaSuccess) ||
         cudaMemcpy(t.d_toff, toff.data(), sizeof(int64_t) * toff.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
-      cudaFree(t.d_rows);
-      cudaFree(t.d_toff);
+      if (t.d_rows) cudaFreeAsync(t.d_rows, nullptr);
+      if (t.d_toff) cudaFreeAsync(t.d_toff, nullptr);
       drop();
       return dm::fail(DM_ERR_OOM, "device allocation for a loaded motif table failed");
     }
@@ -214,8 +216,8 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
     if (t.motif == DM_MOTIF_APEX) {
       dm::ApexTable &ap = g->tabs->apex;
       if (ap.entries >= 0) {  // already built: keep the resident one
-        cudaFree(t.d_rows);
-        cudaFree(t.d_toff);
+        if (t.d_rows) cudaFreeAsync(t.d_rows, nullptr);
+        if (t.d_toff) cudaFreeAsync(t.d_toff, nullptr);
         continue;
       }
       ap.d_apex = t.d_rows;
@@ -226,8 +228,8 @@ dm_status dm_graph_load_motifs(dm_graph *g, const char *path) {
     }
     dm::MotifTable &slot = g->tabs->t[dm::motif_bit(t.motif)];
     if (slot.d_toff) {  // already built: keep the resident one
-      cudaFree(t.d_rows);
-      cudaFree(t.d_toff);
+      if (t.d_rows) cudaFreeAsync(t.d_rows, nullptr);
+      if (t.d_toff) cudaFreeAsync(t.d_toff, nullptr);
       continue;
     }
     t.build_ms = 0.0;

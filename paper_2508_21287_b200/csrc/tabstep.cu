@@ -551,8 +551,9 @@ cudaError_t launch_table(int mode, const DevTabStep &st, const StepIO &io, const
 dm_status finish_motif_table(const dm_graph &g, int32_t *packed, int64_t rows, MotifTable &t, cudaStream_t s) {
   t.stride = row_stride(t.L);
   t.rows = rows;
-  cudaError_t e = cudaMalloc((void **)&t.d_rows, sizeof(int32_t) * (size_t)std::max<int64_t>(rows, 1) * t.stride);
-  if (e == cudaSuccess) e = cudaMalloc((void **)&t.d_toff, sizeof(int64_t) * ((size_t)g.arcs + 1));
+  // graph-owned buffers come from the stream-ordered pool (released by dm_graph_destroy)
+  cudaError_t e = cudaMallocAsync((void **)&t.d_rows, sizeof(int32_t) * (size_t)std::max<int64_t>(rows, 1) * t.stride, s);
+  if (e == cudaSuccess) e = cudaMallocAsync((void **)&t.d_toff, sizeof(int64_t) * ((size_t)g.arcs + 1), s);
   unsigned long long *cnt = nullptr;
   void *tmp = nullptr;
   size_t tb = 0;
@@ -574,8 +575,9 @@ dm_status finish_motif_table(const dm_graph &g, int32_t *packed, int64_t rows, M
   if (cnt) cudaFreeAsync(cnt, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
-    cudaFree(t.d_rows);
-    cudaFree(t.d_toff);
+    if (t.d_rows) cudaFreeAsync(t.d_rows, s);
+    if (t.d_toff) cudaFreeAsync(t.d_toff, s);
+    cudaStreamSynchronize(s);
     t.d_rows = nullptr;
     t.d_toff = nullptr;
     return fail(e == cudaErrorMemoryAllocation ? DM_ERR_OOM : DM_ERR_CUDA,

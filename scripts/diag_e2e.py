@@ -30,5 +30,16 @@ for it in range(6):
     torch.cuda.synchronize()
     t4 = time.perf_counter()
     G.close()
+    torch.cuda.synchronize()
+    t5 = time.perf_counter()
     print(f"graph {1e3*(t1-t0):.2f} ms  motif db {1e3*(t2-t1):.2f} ms  first match {1e3*(t3-t2):.2f} ms  "
-          f"repeat {1e3*(t4-t3):.2f} ms  count {r.count}", flush=True)
+          f"repeat {1e3*(t4-t3):.2f} ms  close {1e3*(t5-t4):.2f} ms  count {r.count}", flush=True)
+# the bench's e2e loop shape: create + lazy motif build inside the first match + close
+for it in range(4):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    G = dm.Graph(n, pin)
+    r = G.match(k, pe, motifs="M2,M7", stream=s)
+    G.close()
+    torch.cuda.synchronize()
+    print(f"e2e step {1e3*(time.perf_counter()-t0):.2f} ms", flush=True)
