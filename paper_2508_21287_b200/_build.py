@@ -27,12 +27,9 @@ def _stale(lib: str) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
-    """libdeltamotif.so, or with checked=True libdeltamotif_checked.so (-DDM_CHECKED)."""
+def _compile(force: bool, verbose: bool, checked: bool):
+    """Start one nvcc per stale translation unit of a variant; returns (lib, objs, procs)."""
     lib = LIB_CHECKED if checked else LIB
-    if not force and not _stale(lib):
-        return lib
-    tmp = lib + f".tmp{os.getpid()}"
     objdir = os.path.join(PKG, "build_checked" if checked else "build")
     os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
@@ -51,14 +48,37 @@ def build(force: bool = False, verbose: bool = False, checked: bool = False) -> 
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         procs.append((subprocess.Popen(cmd), obj))
+    return lib, objs, procs
+
+
+def _link(lib: str, objs, procs):
     for p, obj in procs:
         if p.wait() != 0:
             raise subprocess.CalledProcessError(p.returncode, "nvcc")
         os.replace(obj + ".tmp", obj)
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", *objs, "-o", tmp])
     os.replace(tmp, lib)
     return lib
 
 
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """libdeltamotif.so, or with checked=True libdeltamotif_checked.so (-DDM_CHECKED)."""
+    lib = LIB_CHECKED if checked else LIB
+    if not force and not _stale(lib):
+        return lib
+    return _link(*_compile(force, verbose, checked))
+
+
+def build_all(force: bool = False, verbose: bool = False):
+    """Both variants, every translation unit of both compiling concurrently."""
+    jobs = [_compile(force, verbose, chk) for chk in (False, True)
+            if force or _stale(LIB_CHECKED if chk else LIB)]
+    return [_link(*j) for j in jobs]
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))
+    if "--all" in sys.argv:
+        print(build_all(force="--force" in sys.argv, verbose=True))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kStepThreads) __maxnreg__(MODE == kModeCount ?
   const int ws = row_stride(w);
   const int ss = smem_stride(w);
   const int S = io.slots;
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   int64_t tile;
   if (MODE == kModeSingle) {
     if (tid == 0) s_bc = atomicAdd(io.ctrl + 0, 1ull);
