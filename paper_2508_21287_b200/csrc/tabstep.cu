@@ -348,7 +348,34 @@ __global__ void __launch_bounds__(kStepThreads)
         base = wbase + written;
       }
       __syncwarp();
-      if (base != ~0ull && q < nq) {
+      if (R16 && io.out_elem == 2 && tail_fast) {
+        // 16-bit rows with an aligned tail: two converged passes instead of one divergent one --
+        // the parent-only chunks copied as stored, then the tail chunks packed from the stage
+        if (base != ~0ull) {
+          const int npar = w_al >> 3, ntail = nq - npar;
+          if (npar > 0) {
+            const int rpi_p = 32 / npar, my_o = lane / npar, my_q = lane - my_o * npar;
+            for (int o = my_o; my_o < rpi_p && o < fill; o += rpi_p)
+              reinterpret_cast<uint4 *>(io.out)[(int64_t)(base + o) * nq + my_q] =
+                  *reinterpret_cast<const uint4 *>(rows16 + stage_r[o] * ss + 8 * my_q);
+          }
+          if (ntail > 0) {
+            const int rpi_t = 32 / ntail, my_o = lane / ntail, my_t = lane - my_o * ntail;
+            const int tq = npar + my_t, tc0 = 8 * tq;  // output chunk and its first column
+            for (int o = my_o; my_o < rpi_t && o < fill; o += rpi_t) {
+              const int32_t *nv = sv_new + o * TS + 8 * my_t;
+              uint32_t u[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const uint32_t lo = tc0 + 2 * i < Wn ? (uint32_t)nv[2 * i] & 0xffffu : 0xffffu;
+                const uint32_t hi = tc0 + 2 * i + 1 < Wn ? (uint32_t)nv[2 * i + 1] & 0xffffu : 0xffffu;
+                u[i] = lo | (hi << 16);
+              }
+              reinterpret_cast<uint4 *>(io.out)[(int64_t)(base + o) * nq + tq] = make_uint4(u[0], u[1], u[2], u[3]);
+            }
+          }
+        }
+      } else if (base != ~0ull && q < nq) {
         for (int o = sub; o < fill; o += rpi) {
           const int pr = stage_r[o];
           const int4 neg = make_int4(-1, -1, -1, -1);
