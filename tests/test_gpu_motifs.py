@@ -166,3 +166,25 @@ def test_motif_db_save_load(dm, tmp_path):
     with pytest.raises(dm.DMError) as ei:
         G4.load_motifs(str(tmp_path / "missing.dmdb"))
     assert ei.value.code == -9
+
+
+def test_table_step_two_chunk_tail_16bit(dm):
+    """A materializing M12-O table step on a 16-bit level whose new columns span two output chunks
+    (theta graph of two 12-cycles sharing a 3-vertex path, plus a pendant): the flush packs the
+    staged tail into two 16-byte chunks.  Counts against the oracle, both modes, and tables."""
+    n, e = g.ibm_heavy_hex(6)
+    ed = [(i, (i + 1) % 12) for i in range(12)]
+    chain = [2] + list(range(12, 21)) + [0]
+    ed += [(chain[i], chain[i + 1]) for i in range(len(chain) - 1)]
+    ed.append((6, 21))
+    k, pe = 22, np.array(ed, np.int32)
+    G = dm.Graph(n, e)
+    steps = G.plan(k, pe, motifs="M2,M12-O").describe()["steps"]
+    assert any(st.get("table") == "M12-O" for st in steps[:-1])  # an intermediate table step
+    for mode in ("mono", "induced"):
+        want = oracle.match(n, e, k, pe, table=False, induced=mode == "induced").count
+        for motifs in ("M2,M12-O", "all"):
+            assert G.match(k, pe, mode=mode, motifs=motifs).count == want, (mode, motifs)
+    o = oracle.match(n, e, k, pe)
+    r = G.match(k, pe, output="both", motifs="M2,M12-O")
+    assert r.count == o.count and np.array_equal(r.rows, o.rows)
