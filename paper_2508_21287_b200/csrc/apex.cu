@@ -25,6 +25,7 @@ namespace dm {
 namespace {
 
 constexpr int kApexThreads = 256;
+constexpr int kApexBatch = 4;  // arc rows claimed per atomic by a warp of the 4-clique pair step
 
 __global__ void k_arc_src(const int64_t *__restrict__ off, int32_t n, int32_t *__restrict__ src) {
   const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -118,10 +119,10 @@ __global__ void __launch_bounds__(kStepThreads)
   unsigned long long cnt = 0, cand = 0, probes = 0;
   for (;;) {
     unsigned long long b0 = 0;
-    if (lane == 0) b0 = atomicAdd(row_counter, (unsigned long long)kPairBatch);
+    if (lane == 0) b0 = atomicAdd(row_counter, (unsigned long long)kApexBatch);
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if ((int64_t)b0 >= io.in_rows) break;
-    const int64_t b1 = (int64_t)b0 + kPairBatch < io.in_rows ? (int64_t)b0 + kPairBatch : io.in_rows;
+    const int64_t b1 = (int64_t)b0 + kApexBatch < io.in_rows ? (int64_t)b0 + kApexBatch : io.in_rows;
     for (int64_t r = (int64_t)b0; r < b1; ++r) {
       const int2 ab = __ldg(reinterpret_cast<const int2 *>(io.in + r * 4));
       const int64_t da = degree(off, ab.x), db = degree(off, ab.y);
