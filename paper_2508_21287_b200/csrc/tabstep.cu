@@ -126,8 +126,10 @@ __device__ __forceinline__ void load_tile16(uint16_t *rows, int ss16, int rs16, 
 // the warp's entries are laid out by a warp scan of the per-row entry counts and inspected 32 per
 // round, lane -> entry, the entry's row found by a 5-step shuffle bisection of the row offsets.
 // No CTA barrier between the tile load and the epilogue.  TS = table row stride (4, 8 or 12 ids).
+// Occupancy targets (registers capped by the launch bounds): the count launch fits 6 CTAs per SM
+// in shared memory on 16-bit tiles, the materializing launches 4.
 template <int MODE, bool ELL, int TS, bool R16>
-__global__ void __launch_bounds__(kStepThreads)
+__global__ void __launch_bounds__(kStepThreads, MODE == kModeCount ? 6 : 4)
     k_table(const DevTabStep st, const StepIO io_, const int64_t *__restrict__ off,
             const int32_t *__restrict__ adj, const int32_t *__restrict__ tab,
             const int64_t *__restrict__ toff) {
