@@ -380,10 +380,21 @@ def main():
     psteps = plan.describe()["steps"]
     last_tab = bool(psteps and psteps[-1].get("table"))
     mid_tab = any(st.get("table") for st in psteps[:-1])
+    last = psteps[-1] if psteps else {}
+    new = last.get("new", [])
+    # shared-key pair step: two new vertices, the second keyed on the first's columns (+ maybe it)
+    pair = len(new) == 2 and set(new[1]["nbr_cols"]) - {last["in_w"]} == set(new[0]["nbr_cols"])
+    closing = pair and last["in_w"] in new[1]["nbr_cols"]
     if dom == "join_count":
-        kname = ("k_table (tabstep.cu)" if last_tab else
-                 "k_pairs_apex (apex.cu) / k_pairs (pairs.cu) / k_deep_split (tail.cu) / k_rows, k_step (extend.cu)"
-                 if "apex" in str(motifs) else "k_pairs (pairs.cu) / k_deep_split (tail.cu) / k_rows, k_step (extend.cu)")
+        if last_tab:
+            kname = "k_table (tabstep.cu)"
+        elif pair:
+            kname = "k_pairs_apex (apex.cu)" if closing and "apex" in str(motifs) else "k_pairs (pairs.cu)"
+        elif len(new) >= 3:
+            kname = "k_deep_split (tail.cu)"
+        else:  # row-serial for low-degree graphs (extend.cu: max degree 16 / 4), else candidate-partitioned
+            kname = ("k_rows (extend.cu)" if G.max_degree <= (16 if len(new) == 1 else 4)
+                     else "k_step (extend.cu)")
     else:
         kname = "k_table (tabstep.cu)" if mid_tab else "k_rows / k_step (extend.cu)"
     roof = {"bound": "hbm", "kernel": dom + ": " + kname, "achieved": achieved,
